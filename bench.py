@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""Benchmark of the batched NTT hot path (BASELINE.json metric: NTT butterflies/s and
+achieved HBM GB/s) on B200.
+
+Default workload = BASELINE.json configs[1] (config C2): 4096 transforms of L = 2^12 over
+p = 29*2^57+1 (beta = 2^64), one step = forward + inverse of the whole batch.  Other
+configs (--config c1..c5) are available for measurement; the driver runs the default.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl native|reference]
+
+N > 1: launched by torchrun, one rank per GPU over NCCL; each rank transforms its own
+4096-transform shard (weak scaling, no data-path collective), time = max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P30 = 998244353
+P62 = 29 * 2**57 + 1
+RNS = (469762049, 167772161, 998244353)
+METRIC = "NTT butterflies/s"
+
+CONFIGS = {
+    "c1": dict(workload="C1: 1 x 2^10 forward, beta=2^32, p=998244353", primes=(P30,), bits=32, ell=10, batch=1,
+               ops=("fwd",), scaling="weak", seed_cfg=1),
+    "c2": dict(workload="C2: 4096 x 2^12 forward+inverse, beta=2^64, p=29*2^57+1", primes=(P62,), bits=64, ell=12,
+               batch=4096, ops=("fwd", "inv"), scaling="weak", seed_cfg=2),
+    "c3": dict(workload="C3: 3 primes x 1024 pairs x 2^16 cyclic convolution (fwd,fwd,pointwise,inv), beta=2^32",
+               primes=RNS, bits=32, ell=16, batch=1024, ops=("conv",), scaling="weak", seed_cfg=3),
+    "c4": dict(workload="C4: 64 x 2^24 forward, beta=2^64, p=29*2^57+1", primes=(P62,), bits=64, ell=24, batch=64,
+               ops=("fwd",), scaling="strong", seed_cfg=4),
+    "c5": dict(workload="C5: 1 x 2^28 forward (single GPU four-step), beta=2^64, p=29*2^57+1", primes=(P62,), bits=64,
+               ell=28, batch=1, ops=("fwd",), scaling="weak", seed_cfg=5),
+}
+
+
+def butterflies(cfg, batch):
+    """All (L/2)*ell radix-2 butterflies of Algorithm 1, W = 1 ones included (P:226 divisor)."""
+    L = 1 << cfg["ell"]
+    per = (L // 2) * cfg["ell"]
+    n_ntt = 3 if cfg["ops"] == ("conv",) else len(cfg["ops"])
+    return per * n_ntt * batch * len(cfg["primes"])
+
+
+def root(p, L):
+    return pow(3, (p - 1) // L, p)
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ native arm
+def run_native(args, cfg, rank, world, local_rank):
+    import torch
+    import paper_1205_2926_b200 as ntt
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    L = 1 << cfg["ell"]
+    bits = cfg["bits"]
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    wb = bits // 8
+    batch = cfg["batch"]
+    if cfg["scaling"] == "strong" and world > 1:
+        assert batch % world == 0, "strong-scaled batch must divide over ranks"
+        batch //= world
+    plans = [ntt.Plan(p, root(p, L), cfg["ell"], bits, device=local_rank) for p in cfg["primes"]]
+    conv = cfg["ops"] == ("conv",)
+    # inputs generated in HBM by the seeded counter-based generator (synth/ definition)
+    seed = 0x12052926 ^ cfg["seed_cfg"]
+    first = rank * batch
+    with torch.cuda.stream(stream):
+        if conv:
+            half = L // 2
+            a0 = torch.zeros(batch, L, dtype=dt, device=dev)
+            b0 = torch.zeros(batch, L, dtype=dt, device=dev)
+            tmp = torch.empty(batch * half, dtype=dt, device=dev)
+            ntt.synth_uniform(tmp, seed, 0, start=first * half, bits=20, stream=stream)
+            a0[:, :half] = tmp.view(batch, half)
+            ntt.synth_uniform(tmp, seed, 1, start=first * half, bits=20, stream=stream)
+            b0[:, :half] = tmp.view(batch, half)
+            del tmp
+            work = [(a0.clone(), b0.clone()) for _ in plans]
+            src = (a0, b0)
+        else:
+            x0 = torch.empty(batch * L, dtype=dt, device=dev)
+            ntt.synth_uniform(x0, seed, 0, start=first * L, bound=cfg["primes"][0], stream=stream)
+            x = x0.clone()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream.synchronize()
+
+    def step(evs=None):
+        """One step: the whole hot path over this rank's batch.  evs: events between launches."""
+        launches = 0
+        if conv:
+            for pl, (a, b) in zip(plans, work):
+                pl.cyclic_convolve(a, b, stream=stream)
+                launches += ntt.last_launch_count()
+                if evs is not None:
+                    evs.append(("conv", torch.cuda.Event(enable_timing=True)))
+                    evs[-1][1].record(stream)
+        else:
+            for op in cfg["ops"]:
+                (plans[0].forward if op == "fwd" else plans[0].inverse)(x, stream=stream)
+                launches += ntt.last_launch_count()
+                if evs is not None:
+                    evs.append((op, torch.cuda.Event(enable_timing=True)))
+                    evs[-1][1].record(stream)
+        return launches
+
+    def reset_inputs():
+        with torch.cuda.stream(stream):
+            if conv:
+                for a, b in work:
+                    a.copy_(src[0]); b.copy_(src[1])
+            else:
+                x.copy_(x0)
+
+    # ---- ALU roofline peak, measured live: register-only Alg. 3 butterflies
+    p0 = cfg["primes"][0]
+    W0 = root(p0, 4)
+    sink = torch.zeros(4, dtype=torch.int64, device=dev)
+    calib = []
+    for it in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = ntt.calibrate_butterfly(bits, p0, W0, (W0 << bits) // p0, 2048 if bits == 64 else 8192, sink,
+                                    stream=stream)
+        e1.record(stream)
+        stream.synchronize()
+        if it:
+            calib.append(n / (e0.elapsed_time(e1) * 1e-3))
+    alu_peak = max(calib)
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        reset_inputs()
+        step()
+    stream.synchronize()
+
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    step_ms, kernel_ms, launches = [], {}, 0
+    for _ in range(args.steps):
+        reset_inputs()
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        evs = []
+        launches += step(evs)
+        stream.synchronize()
+        prev = start
+        for name, ev in evs:
+            kernel_ms.setdefault(name, []).append(prev.elapsed_time(ev))
+            prev = ev
+        step_ms.append(start.elapsed_time(evs[-1][1]))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    bfly_rank = butterflies(cfg, batch)
+    value = bfly_rank * world * args.steps / (total_ms * 1e-3)
+
+    # ---- dominant kernel (largest share of the step) and its roofline
+    share = {k: sum(v) for k, v in kernel_ms.items()}
+    dom = max(share, key=share.get)
+    dom_ms = statistics.mean(kernel_ms[dom])
+    per_launch_bfly = butterflies(cfg, batch) // (len(plans) if conv else len(cfg["ops"]))
+    if conv:
+        per_launch_bfly = butterflies(cfg, batch) // len(plans)  # one cyclic convolution (3 NTTs) per prime
+    passes = plans[0].info().n_passes
+    # algorithmic HBM bytes per launch: one read + one write of the data per pass
+    if conv:
+        alg_bytes = (2 * batch * L * wb) * (2 * passes) + 3 * batch * L * wb + 2 * batch * L * wb * passes
+    else:
+        alg_bytes = 2 * batch * L * wb * passes
+    achieved_bfly = per_launch_bfly / (dom_ms * 1e-3)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {
+        "bound": "alu",
+        "kernel": f"{dom} ({'fused single-pass' if passes == 1 else f'{passes}-pass four-step'})",
+        "achieved": round(achieved_bfly / 1e9, 2),
+        "peak": round(alu_peak / 1e9, 2),
+        "unit": "Gbutterflies/s",
+        "frac": round(achieved_bfly / alu_peak, 4),
+        "peak_source": "live register-only Alg.3 butterfly loop (ntt_calibrate_butterfly), same process/clocks",
+        "traffic": traffic,
+        "hbm": {"achieved_GBps": round(alg_bytes / (dom_ms * 1e-3) / 1e9, 1), "peak_GBps": hbm_peak,
+                "frac": round(alg_bytes / (dom_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
+                "algorithmic_bytes_per_launch": alg_bytes},
+    }
+
+    # ---- e2e: the same step through the C-ABI host-buffer call (ntt_execute_host),
+    # H2D of the inputs and D2H of the results inside the timed region
+    e2e = None
+    if not conv:
+        ops = 0
+        for op in cfg["ops"]:
+            ops |= ntt.NTT_OP_FORWARD if op == "fwd" else ntt.NTT_OP_INVERSE
+        h_in = torch.empty(batch * L, dtype=dt, pin_memory=True)
+        h_in.copy_(x0.cpu())
+        h_out = torch.empty_like(h_in).pin_memory()
+        dbuf = torch.empty(max(L, min(batch * L, (64 << 20) // wb)), dtype=dt, device=dev)
+        for _ in range(2):
+            plans[0].execute_host(ops, h_in, h_out, dbuf, stream=stream)
+        stream.synchronize()
+        ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plans[0].execute_host(ops, h_in, h_out, dbuf, stream=stream)
+            e1.record(stream)
+            stream.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        e2e_ms = sum(ms)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": bfly_rank * world * len(ms) / (e2e_ms * 1e-3), "unit": "butterflies/s",
+               "h2d_bytes_per_step": batch * L * wb, "d2h_bytes_per_step": batch * L * wb,
+               "api": "ntt_execute_host (pinned host in/out, chunked H2D/compute/D2H pipeline)"}
+    else:
+        # C3 end to end: host a,b -> device, 3 convolutions, residues back
+        h_a = src[0].cpu().pin_memory()
+        h_b = src[1].cpu().pin_memory()
+        h_out = torch.empty((len(plans),) + tuple(h_a.shape), dtype=dt).pin_memory()
+        ms = []
+        for it in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            with torch.cuda.stream(stream):
+                for i, (pl, (a, b)) in enumerate(zip(plans, work)):
+                    a.copy_(h_a, non_blocking=True)
+                    b.copy_(h_b, non_blocking=True)
+                    pl.cyclic_convolve(a, b, stream=stream)
+                    h_out[i].copy_(a, non_blocking=True)
+            e1.record(stream)
+            stream.synchronize()
+            if it:
+                ms.append(e0.elapsed_time(e1))
+        e2e = {"value": bfly_rank * world * len(ms) / (sum(ms) * 1e-3), "unit": "butterflies/s",
+               "h2d_bytes_per_step": 2 * batch * L * wb * len(plans),
+               "d2h_bytes_per_step": batch * L * wb * len(plans),
+               "api": "torch pinned copies + ntt_cyclic_convolve per prime"}
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "butterflies/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "u64" if bits == 64 else "u32",
+            "data": "synthetic: seeded counter-based uniform residues generated in HBM (synth/ definition)",
+            "config": {"workload": cfg["workload"], "transforms_per_gpu": batch, "L": L,
+                       "butterflies_per_step_per_gpu": bfly_rank,
+                       "parallelism": f"batch-sharded x{world}, no collective",
+                       "passes": passes,
+                       "l2": "flushed between timed steps (256 MiB zero-fill, outside the step events)"},
+            "hbm_GBps": round(2 * batch * L * wb * passes * (len(cfg['ops']) if not conv else 3 * len(plans))
+                              * world * args.steps / (total_ms * 1e-3) / 1e9, 1),
+            "roofline": roofline,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "kernel_ms_mean": {k: round(statistics.mean(v), 4) for k, v in kernel_ms.items()},
+        }
+    return out
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def oracle_sample(cfg):
+    """Bounded sample of the workload for the CPU oracle: (transforms, seconds-sized)."""
+    return {"c1": 1, "c2": 4096, "c3": 1, "c4": 1, "c5": 1}[cfg["key"]]
+
+
+def run_oracle_steps(cfg, steps, warmup, nthreads):
+    """The oracle (oracle/, plain Alg. 1 with 128-bit %) on a bounded sample of the workload."""
+    import numpy as np
+
+    import oracle
+    import synth
+    L = 1 << cfg["ell"]
+    seed = synth.config_seed(cfg["seed_cfg"])
+    if cfg["key"] == "c5":  # a 2^28 transform is ~45 thread-seconds: use a 2^24 prefix-sized sample
+        ell = 24
+    else:
+        ell = cfg["ell"]
+    Ls = 1 << ell
+    nb = oracle_sample(cfg)
+    if cfg["ops"] == ("conv",):
+        half = Ls // 2
+        a = np.zeros((nb, Ls), dtype=np.uint64)
+        b = np.zeros((nb, Ls), dtype=np.uint64)
+        a[:, :half] = synth.uniform_bits(seed, 0, 0, nb * half, 20).reshape(nb, half)
+        b[:, :half] = synth.uniform_bits(seed, 1, 0, nb * half, 20).reshape(nb, half)
+    else:
+        x = synth.uniform_mod(seed, 0, 0, nb * Ls, cfg["primes"][0]).reshape(nb, Ls)
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        for p in cfg["primes"]:
+            w = root(p, Ls)
+            if cfg["ops"] == ("conv",):
+                fa = oracle.ntt_forward(p, w, a, nthreads=nthreads)
+                fb = oracle.ntt_forward(p, w, b, nthreads=nthreads)
+                oracle.ntt_inverse(p, w, oracle.pointwise(p, fa, fb, scale_L=Ls), nthreads=nthreads)
+            else:
+                y = x
+                for op in cfg["ops"]:
+                    y = (oracle.ntt_forward if op == "fwd" else oracle.ntt_inverse)(p, w, y, nthreads=nthreads)
+        if it >= warmup:
+            times.append(time.perf_counter() - t0)
+    n_ntt = 3 if cfg["ops"] == ("conv",) else len(cfg["ops"])
+    bfly = (Ls // 2) * ell * n_ntt * nb * len(cfg["primes"])
+    value = bfly * len(times) / sum(times)
+    sample = (f"{nb} transform(s) of 2^{ell} x {n_ntt} NTT(s) x {len(cfg['primes'])} prime(s) per step"
+              + (" (2^24 stands in for the 2^28 transform)" if cfg["key"] == "c5" else ""))
+    return value, sample, sum(times) / len(times)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = dict(CONFIGS[args.config], key=args.config)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    nthreads = len(os.sched_getaffinity(0))
+
+    if args.impl == "reference":
+        # The reference arm is the CPU oracle (there is no reference implementation to
+        # install).  Rank 0 only; other ranks exit without work.
+        if rank != 0:
+            return
+        value, sample, sec = run_oracle_steps(cfg, args.steps, args.warmup, nthreads)
+        out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "butterflies/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+               "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "u64" if cfg["bits"] == 64 else "u32",
+               "data": "synthetic: seeded counter-based uniform residues (synth/ definition)",
+               "config": {"workload": cfg["workload"]},
+               "cpu_baseline": {"value": value, "unit": "butterflies/s", "cores": nthreads, "kind": "oracle",
+                                "sample": sample, "cpu": cpu_model()},
+               "e2e": {"value": value, "unit": "butterflies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_native(args, cfg, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            value, sample, _ = run_oracle_steps(cfg, 1, 0, nthreads)
+            out["cpu_baseline"] = {"value": value, "unit": "butterflies/s", "cores": nthreads, "kind": "oracle",
+                                   "sample": sample, "cpu": cpu_model()}
+        elif world > 1:
+            out["cpu_baseline"] = None
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * ntt_b200.h -- C ABI of the B200-native batched NTT engine.
+ *
+ * Implements the hot path of D. Harvey, "Faster arithmetic for number-theoretic
+ * transforms" (arXiv:1205.2926): the radix-2 NTT over F_p (Algorithm 1, PAPER.md
+ * P:27-46) with the lazy Shoup butterfly (Algorithm 3; operands in
+ * [0,2p)) for the forward transform and the lazy inverse butterfly (Algorithm 4,
+ * P:142-159; operands in [0,4p)) for the inverse, W' = floor(W beta / p).
+ * Citations: P:n = line n of the paper text.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - beta (the machine word) is 2^32 or 2^64.  Data words are uint32_t for
+ *   beta = 2^32 and uint64_t for beta = 2^64, in DEVICE memory owned by the
+ *   caller, batch x L words, contiguous, transform b at offset b*L, 16-byte
+ *   aligned.  The library never allocates in a transform call.
+ * - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *   stream) and are stream-ordered.  Argument and plan errors are reported
+ *   synchronously; an asynchronous CUDA fault surfaces as NTT_ERR_CUDA from a
+ *   later call or a stream synchronisation.  No C++ exception crosses the ABI.
+ * - Input ranges are preconditions (not checked in the hot path): forward
+ *   needs x < 2p (Alg. 3 input), inverse needs x < 4p (Alg. 4).
+ * - Outputs are always normalised to [0,p) ("normalise the final NTT
+ *   output"); bit-exactness is defined on these canonical values.
+ * - A plan is immutable after creation and may be shared by threads and
+ *   streams; distinct buffers may be transformed concurrently with one plan.
+ */
+#ifndef NTT_B200_H
+#define NTT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ntt_plan_s* ntt_plan_t;   /* opaque */
+typedef struct CUstream_st* ntt_stream_t; /* identical to cudaStream_t */
+
+typedef enum {
+  NTT_OK = 0,
+  NTT_ERR_ARG = -1,         /* null pointer, misaligned buffer, size overflow, bad flag */
+  NTT_ERR_MODULUS = -2,     /* p even, composite, or p >= beta/4 (Alg. 3/4 precondition) */
+  NTT_ERR_ROOT = -3,        /* omega^(L/2) != p-1, i.e. omega is not a primitive L-th root */
+  NTT_ERR_LENGTH = -4,      /* ell > 28, or 2^ell does not divide p-1 ("p = 1 mod L") */
+  NTT_ERR_WORD = -5,        /* log2_beta not in {32, 64} */
+  NTT_ERR_CUDA = -6,        /* a CUDA runtime error (see ntt_last_cuda_error) */
+  NTT_ERR_NOMEM = -7,       /* device or host allocation failed at plan creation */
+  NTT_ERR_UNSUPPORTED = -8  /* valid request this build does not implement */
+} ntt_status;
+
+/* ntt_pointwise_mul flags */
+#define NTT_SCALE_INV_L 1u /* multiply the products by L^{-1} mod p */
+
+/* Plan: validates (p, omega, ell, beta) and precomputes the twiddle tables
+ * W = omega^e, W' = floor(W beta / p) ("precomputed and reused").
+ *   p         : odd prime, p < beta/4, p = 1 mod 2^ell
+ *   omega     : primitive 2^ell-th root of unity mod p; checked as omega^(L/2) = p-1
+ *   ell       : transform length L = 2^ell, 0 <= ell <= 28 (ell = 0 is the identity)
+ *   log2_beta : 32 or 64 (word size)
+ *   device    : CUDA device ordinal that owns the plan's tables
+ * On success *out owns device tables on `device` (free with ntt_plan_destroy).
+ * On error *out is set to NULL. */
+ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta, int device);
+ntt_status ntt_plan_destroy(ntt_plan_t plan);
+
+typedef struct {
+  uint64_t p, omega, omega_inv, L_inv; /* L_inv = L^{-1} mod p */
+  unsigned ell, log2_beta, word_bytes;
+  unsigned n_passes;                   /* kernel passes per transform on one GPU (1 = fused on chip) */
+  unsigned pass_log2[4];               /* log2 of each pass's sub-transform length, outermost first */
+  int device;
+} ntt_plan_info_t;
+ntt_status ntt_plan_info(ntt_plan_t plan, ntt_plan_info_t* out);
+
+/* Forward NTT, in place (Algorithm 1, with the Algorithm 3 butterfly):
+ * natural-order input in [0,2p) -> output j = b_{rev(j)} (bit-reversed),
+ * b_k = sum_i omega^{ik} a_i, normalised to [0,p).
+ *   x     : device pointer, batch*L words
+ *   batch : number of independent transforms (0 is a no-op) */
+ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream);
+
+/* Inverse NTT, in place: Algorithm 1 run backwards with the Algorithm 4
+ * butterfly and twiddles omega^{-k}: bit-reversed input in [0,4p) -> natural
+ * order, UNSCALED (ntt_inverse(ntt_forward(a)) = L*a mod p), normalised to [0,p). */
+ntt_status ntt_inverse(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream);
+
+/* Pointwise product for the convolution use: c_k = a_k b_k [* L^{-1}]
+ * mod p for k < batch*L.  Inputs in [0,2p); output canonical [0,p).  c may
+ * alias a or b. */
+ntt_status ntt_pointwise_mul(ntt_plan_t plan, void* c, const void* a, const void* b, size_t batch, unsigned flags,
+                             ntt_stream_t stream);
+
+/* Cyclic convolution of `batch` pairs (config C3 building block): a <- a * b
+ * (cyclic, length L, mod p).  Runs forward(a), forward(b), pointwise with
+ * L^{-1}, inverse(a); b is overwritten by its transform.  Inputs in [0,2p). */
+ntt_status ntt_cyclic_convolve(ntt_plan_t plan, void* a, void* b, size_t batch, ntt_stream_t stream);
+
+/* Host-resident data (end-to-end use): ops is a bit set of NTT_OP_FORWARD and
+ * NTT_OP_INVERSE (forward first when both).  host_in / host_out hold batch*L words
+ * in HOST memory (page-locked for overlap; pageable works but serialises);
+ * host_out may equal host_in.  dev_buf is caller-owned DEVICE scratch of
+ * dev_buf_bytes >= L*word_bytes: the batch is streamed through it in chunks,
+ * each chunk's H2D copy, transform(s) and D2H copy pipelined over the plan's own
+ * streams so copies overlap compute.  Ordered after prior work on `stream`;
+ * later work on `stream` waits for the whole call. */
+#define NTT_OP_FORWARD 1u
+#define NTT_OP_INVERSE 2u
+ntt_status ntt_execute_host(ntt_plan_t plan, unsigned ops, const void* host_in, void* host_out, size_t batch,
+                            void* dev_buf, size_t dev_buf_bytes, ntt_stream_t stream);
+
+/* Copy the plan's forward twiddle table W_e = omega^e, W'_e = floor(W_e beta/p),
+ * e < L/2, to host arrays of L/2 words each (test hook; W' check P:85).
+ * Returns NTT_ERR_UNSUPPORTED when ell > 20 (tables are factored then). */
+ntt_status ntt_plan_twiddles(ntt_plan_t plan, void* host_W, void* host_Wp);
+
+/* ---- four-step pass entry points for a transform split over G GPUs (config C5) ----
+ * View the length-L transform (L = 2^ell) as an N1 x N2 row-major matrix,
+ * N1 = 2^ell1, N2 = L/N1, M[r][c] = x[N2 r + c].  Rank g of G holds the column
+ * shard c in [g N2/G, (g+1) N2/G) as an N1 x (N2/G) row-major matrix.
+ *   ntt_fourstep_cols: length-N1 NTTs down every local column (root omega^{N2}),
+ *     then M[r][c] *= omega^{c rev_{ell1}(r)} (four-step twiddle); output in
+ *     [0,2p).  This is stages 1..ell1 of Algorithm 1, re-associated.
+ *   ntt_fourstep_rows: input `recv` holds G blocks; block h (h < G) is the
+ *     (N1/G) x (N2/G) sub-matrix rows [g N1/G, (g+1) N1/G) x columns
+ *     [h N2/G, (h+1) N2/G), row-major, blocks back to back (the all-to-all
+ *     receive layout).  Runs length-N2 NTTs on the N1/G full rows (root
+ *     omega^{N1}) and writes them, normalised, to `out` (N1/G x N2, row major):
+ *     out = flat positions [g L/G, (g+1) L/G) of Algorithm 1's bit-reversed output.
+ * Both need ell1 = ell/2 (ell even), G a power of two dividing N1 and N2/16. */
+ntt_status ntt_fourstep_cols(ntt_plan_t plan, unsigned ell1, void* x_shard, unsigned rank, unsigned world,
+                             ntt_stream_t stream);
+ntt_status ntt_fourstep_rows(ntt_plan_t plan, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,
+                             ntt_stream_t stream);
+
+/* Seeded counter-based generator (test/bench infrastructure; same definition as
+ * synth/__init__.py): x[i] = element (start+i) of stream (seed, tensor_id),
+ * uniform in [0, bound) by rejection if bound != 0, else uniform in [0, 2^bits).
+ * word_bytes = 4 or 8. */
+ntt_status ntt_synth_uniform(void* x, size_t count, unsigned word_bytes, uint64_t seed, uint64_t tensor_id,
+                             uint64_t start, uint64_t bound, unsigned bits, ntt_stream_t stream);
+
+/* Debug/ablation hook: run one butterfly algorithm of the paper element-wise on
+ * device arrays (alg 2 = Algorithm 2, 3 = Algorithm 3, 4 = Algorithm 4,
+ * 5 = Algorithm 5 with Wp = beta W mod p and J = p^{-1} mod beta, 31 = the W = 1
+ * fast path of Algorithm 3).  All arrays hold n words of the plan's width. */
+ntt_status ntt_debug_butterfly(ntt_plan_t plan, int alg, const void* W, const void* Wp, void* X, void* Y, size_t n,
+                               ntt_stream_t stream);
+
+/* ALU-roofline calibration (bench infrastructure): launches a register-only loop of
+ * Algorithm 3 butterflies -- no memory traffic -- so that the caller can
+ * time the sustained butterfly rate of the integer pipes at the live clocks.
+ * *n_butterflies receives the number of butterflies the launch performs.
+ * sink: device buffer of >= 16 bytes (defeats dead-code elimination). */
+ntt_status ntt_calibrate_butterfly(unsigned log2_beta, uint64_t p, uint64_t W, uint64_t Wp, unsigned iters,
+                                   void* sink, uint64_t* n_butterflies, ntt_stream_t stream);
+
+/* Number of kernel launches the last transform entry point on this thread issued. */
+unsigned ntt_last_launch_count(void);
+const char* ntt_status_str(ntt_status s);
+const char* ntt_last_cuda_error(void);
+unsigned ntt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTT_B200_H */

@@ -54,6 +54,8 @@ def _load():
         lib.orc_cyclic_conv_coeff.restype = u64
         lib.orc_cyclic_conv_coeff.argtypes = [u64, U64P, U64P, u64, u64]
         lib.orc_schoolbook_mod.argtypes = [u64, U64P, u64, U64P, u64, U64P]
+        lib.orc_poly_eval.restype = u64
+        lib.orc_poly_eval.argtypes = [u64, U64P, u64, u64]
         lib.orc_bfly_batch.restype = c_int
         lib.orc_bfly_batch.argtypes = [c_int, c_uint, u64, u64, u64, U64P, U64P, U64P, U64P, U64P, U64P]
         _lib = lib
@@ -133,6 +135,20 @@ def schoolbook_mod(p: int, a, b) -> np.ndarray:
     out = np.zeros(a.size + b.size - 1, dtype=np.uint64)
     _load().orc_schoolbook_mod(p, _ptr(a), a.size, _ptr(b), b.size, _ptr(out))
     return out
+
+
+def poly_eval(p: int, a, x: int) -> int:
+    """P:24 (evaluation form): a(x) mod p by Horner."""
+    a = _u64(a)
+    return int(_load().orc_poly_eval(p, _ptr(a), a.size, x))
+
+
+def ntt_output_at(p: int, omega: int, a, j: int) -> int:
+    """Algorithm 1 output position j (bit-reversed order) = a(omega^{rev(j)})."""
+    a = _u64(a)
+    ell = a.size.bit_length() - 1
+    rj = int(format(j, f"0{ell}b")[::-1], 2) if ell else 0
+    return poly_eval(p, a, powmod(omega, rj, p))
 
 
 def bfly(alg: int, bb: int, p: int, W, Wp, X, Y, J: int = 0):

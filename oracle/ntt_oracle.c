@@ -297,3 +297,11 @@ int orc_bfly_batch(int alg, unsigned bb, uint64_t p, uint64_t J, uint64_t n, con
     if (orc_bfly(alg, bb, p, W[i], Wp[i], J, X[i], Y[i], &Xo[i], &Yo[i])) return -1;
   return 0;
 }
+
+/* P:24, second form: the NTT evaluates a(x) = a_0 + a_1 x + ... + a_{L-1} x^{L-1}
+ * at the powers of omega.  Horner evaluation of a(x) mod p, O(L). */
+uint64_t orc_poly_eval(uint64_t p, const uint64_t* a, uint64_t L, uint64_t x) {
+  uint64_t acc = 0;
+  for (uint64_t i = L; i-- > 0;) acc = addmod(mulmod(acc, x % p, p), a[i] % p, p);
+  return acc;
+}

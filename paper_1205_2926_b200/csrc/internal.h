@@ -1,0 +1,63 @@
+// internal.h -- declarations shared by the host plan code (plan.cu) and the
+// kernel launchers (ntt_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nttb {
+
+// Limits of the on-chip (single-pass) transform and of the column pass, as
+// log2 of the sub-transform length, per word size.
+constexpr int kContigMaxLog64 = 14;  // 2^14 u64 = 128 KiB smem, 512 threads x 32 words
+constexpr int kContigMaxLog32 = 15;  // 2^15 u32 = 128 KiB smem, 1024 threads x 32 words
+constexpr int kColsMaxLog64 = 9;     // 2^9 rows x 16 u64 columns = 64 KiB tile
+constexpr int kColsMaxLog32 = 10;    // 2^10 rows x 32 u32 columns = 128 KiB tile
+constexpr int kColsMinLog = 4;
+
+// Column-pass geometry (four-step pass j of the nested decomposition):
+// the data is viewed as blocks of B = N*S words; inside a block, element
+// (row r < N, column c < S) sits at r*S + c.  The pass runs length-N NTTs down
+// every column and (forward) multiplies element (r, c) by omega_L^{e},
+// e = (c * rev_logN(r)) << log_tw_mul, or (inverse) by omega_L^{-e} first.
+struct ColsParams {
+  uint64_t n_tiles;        // (#blocks) * (S / C)
+  uint32_t log_S;          // row stride within a block (words)
+  uint32_t log_colgroups;  // log2(S / C)
+  uint32_t log_tw_mul;     // log2(L / B): converts block-root exponents to omega_L exponents
+  uint32_t ell;            // log2 L
+  uint32_t H;              // factored-table split (0 = direct table of L entries)
+  uint32_t twiddle;        // 0: no four-step twiddle; 1: apply it
+  uint32_t normalize;      // 1: write canonical [0,p) output
+  // distributed shard (config C5): global column = col_map(local column)
+  uint32_t shard;          // 0: plain; 1: local columns map to global via the fields below
+  uint32_t log_local_w;    // log2 of the local matrix width (N2/G)
+  uint32_t log_n2;         // log2 N2 (global width)
+  uint32_t col0;           // first global column of this shard
+};
+
+struct DevTables {
+  const void* sub_fwd;  // omega_N^e, e < N/2, pairs (W, W')
+  const void* sub_inv;  // omega_N^{-e}
+  const void* fa;       // factored four-step table A (or the direct table when H == 0)
+  const void* fb;       // factored four-step table B
+};
+
+// launchers (return cudaGetLastError of the launch)
+cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch, const void* tw,
+                          uint64_t p, cudaStream_t s);
+cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
+                        uint64_t p, cudaStream_t s);
+cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
+                               uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s);
+cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, size_t n, uint64_t p, uint64_t J,
+                             uint64_t K, uint64_t Kp, cudaStream_t s);
+cudaError_t launch_normalize(int wbytes, void* x, size_t n, uint64_t p, int from4p, cudaStream_t s);
+cudaError_t launch_synth(int wbytes, void* x, size_t count, uint64_t seed, uint64_t tensor_id, uint64_t start,
+                         uint64_t bound, unsigned bits, cudaStream_t s);
+cudaError_t launch_calib(int wbytes, uint64_t p, uint64_t w, uint64_t wp, unsigned iters, void* sink,
+                         uint64_t* n_bfly, cudaStream_t s);
+cudaError_t launch_debug_bfly(int wbytes, int alg, const void* W, const void* Wp, void* X, void* Y, size_t n,
+                              uint64_t p, uint64_t J, cudaStream_t s);
+
+}  // namespace nttb

@@ -1,0 +1,112 @@
+// modarith.cuh -- word arithmetic and the paper's butterflies on sm_100a.
+//
+// Word type W is uint32_t (beta = 2^32) or uint64_t (beta = 2^64).  Every
+// function is branch-free: the conditional corrections compile to ISETP+SEL
+// (P:93 prefers conditional moves to branches).  Citations P:n = PAPER.md line n.
+#pragma once
+#include <cstdint>
+
+namespace nttb {
+
+template <class W> struct TwPair;               // (W, W') twiddle pair, stored adjacently
+template <> struct alignas(8) TwPair<uint32_t> { uint32_t w, wp; };
+template <> struct alignas(16) TwPair<uint64_t> { uint64_t w, wp; };
+
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+__device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+template <class W> __device__ __forceinline__ W csub(W x, W m) { return x >= m ? x - m : x; }
+
+// Shoup multiplication (Theorem 1 bound P:85): for any T < beta,
+// returns WT - Qp in [0, 2p), congruent to W*T mod p, Q = floor(W'T/beta).
+template <class W> __device__ __forceinline__ W shoup_mul(W T, W w, W wp, W p) {
+  W Q = mulhi(wp, T);
+  return w * T - Q * p;  // mod beta
+}
+
+// Algorithm 3, the modified Shoup butterfly:
+// X, Y in [0,2p) -> X' = X+Y, Y' = W(X-Y), both in [0,2p)  (Theorem 2).
+template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, W p, W p2) {
+  W s = csub<W>(X + Y, p2);   // lines 1-2
+  W T = X - Y + p2;           // line 3: T in [0,4p), no correction
+  Y = shoup_mul<W>(T, w, wp, p);  // lines 4-5: [0,2p), no correction
+  X = s;
+}
+
+// W = 1 butterflies (O(L) butterflies have W = 1 and are cheaper):
+// X' as in Alg. 3, Y' = T reduced once by 2p, so Y' in [0,2p), no multiply.
+template <class W> __device__ __forceinline__ void bfly_alg3_w1(W& X, W& Y, W p2) {
+  W s = csub<W>(X + Y, p2);
+  W T = csub<W>(X - Y + p2, p2);
+  X = s;
+  Y = T;
+}
+
+// Algorithm 4, the modified inverse butterfly:
+// X, Y in [0,4p) -> X' = X + WY, Y' = X - WY, both in [0,4p)  (Theorem 3).
+template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, W p, W p2) {
+  W x = csub<W>(X, p2);            // line 1
+  W T = shoup_mul<W>(Y, w, wp, p);  // lines 2-3: Y < 4p < beta is a legal Shoup input
+  X = x + T;
+  Y = x - T + p2;
+}
+
+// W = 1 inverse butterfly: T = Y reduced once by 2p (Y < 4p -> T < 2p).
+template <class W> __device__ __forceinline__ void bfly_alg4_w1(W& X, W& Y, W p2) {
+  W x = csub<W>(X, p2);
+  W T = csub<W>(Y, p2);
+  X = x + T;
+  Y = x - T + p2;
+}
+
+// Algorithm 2, NTL's butterfly, canonical [0,p) in and out (ablation F1).
+// "if T < 0" is realised as X < Y.
+template <class W> __device__ __forceinline__ void bfly_alg2(W& X, W& Y, W w, W wp, W p) {
+  W s = csub<W>(X + Y, p);
+  W T = (X < Y) ? X - Y + p : X - Y;
+  W r = csub<W>(shoup_mul<W>(T, w, wp, p), p);
+  X = s;
+  Y = r;
+}
+
+// Full product hi/lo for Algorithm 5.
+__device__ __forceinline__ void mul_wide(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+  uint64_t r = (uint64_t)a * b;
+  hi = (uint32_t)(r >> 32);
+  lo = (uint32_t)r;
+}
+__device__ __forceinline__ void mul_wide(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
+  hi = __umul64hi(a, b);
+  lo = a * b;
+}
+
+// Algorithm 5, the modified Montgomery butterfly; wm = beta W mod p,
+// J = p^{-1} mod beta.  X, Y in [0,2p) -> [0,2p)  (Theorem 4).
+template <class W> __device__ __forceinline__ void bfly_alg5(W& X, W& Y, W wm, W J, W p, W p2) {
+  W s = csub<W>(X + Y, p2);
+  W T = X - Y + p2;
+  W R1, R0;
+  mul_wide(wm, T, R1, R0);  // line 4
+  W Q = R0 * J;             // line 5
+  W H = mulhi(Q, p);        // line 6
+  Y = R1 - H + p;           // line 7
+  X = s;
+}
+
+// Final normalisation: [0,2p) -> [0,p) and [0,4p) -> [0,p).
+template <class W> __device__ __forceinline__ W norm2(W x, W p) { return csub<W>(x, p); }
+template <class W> __device__ __forceinline__ W norm4(W x, W p, W p2) { return csub<W>(csub<W>(x, p2), p); }
+
+// Pointwise product of two data values (no reusable W', so no Shoup; P:21 use):
+// returns a*b*R^{-1}-style Montgomery REDC in the Alg. 5 pattern:
+// for a, b < 2p: ab < 4p^2 < p beta, so R1 < p and the result lies in (0, 2p),
+// congruent to a b beta^{-1} mod p.
+template <class W> __device__ __forceinline__ W mont_redc_mul(W a, W b, W J, W p) {
+  W R1, R0;
+  mul_wide(a, b, R1, R0);
+  W Q = R0 * J;
+  W H = mulhi(Q, p);
+  return R1 - H + p;
+}
+
+}  // namespace nttb

@@ -1,0 +1,632 @@
+// ntt_kernels.cu -- sm_100a kernels of the batched NTT engine.
+//
+// Algorithm 1 is executed as "rounds": a thread holds
+// E = 2^LE words in registers and runs up to LE consecutive radix-2 stages on
+// them (the lazy butterflies of modarith.cuh); between rounds the CTA exchanges
+// data through an XOR-swizzled shared-memory tile.  The first round reads HBM
+// directly into registers (coalesced across lanes) and the last round writes
+// back (vectorised), so a transform that fits on chip costs one HBM read and one
+// HBM write.  Longer transforms use the nested four-step schedule of DESIGN.md
+// (column passes with the fused twiddle, then a contiguous row pass).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+#include "modarith.cuh"
+
+namespace nttb {
+
+// ----------------------------------------------------------------- helpers
+template <class W> __device__ __forceinline__ void ldtw(const TwPair<W>* tw, uint32_t e, W& w, W& wp);
+template <> __device__ __forceinline__ void ldtw<uint64_t>(const TwPair<uint64_t>* tw, uint32_t e, uint64_t& w,
+                                                           uint64_t& wp) {
+  ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(tw) + e);
+  w = t.x;
+  wp = t.y;
+}
+template <> __device__ __forceinline__ void ldtw<uint32_t>(const TwPair<uint32_t>* tw, uint32_t e, uint32_t& w,
+                                                           uint32_t& wp) {
+  uint2 t = __ldg(reinterpret_cast<const uint2*>(tw) + e);
+  w = t.x;
+  wp = t.y;
+}
+
+// XOR swizzle of the word index inside a 128-byte smem row, so that the
+// strided exchange patterns of every round hit distinct banks.
+template <class W> __device__ __forceinline__ int swz(int i) {
+  constexpr int S = sizeof(W) == 8 ? 4 : 5;
+  return i ^ ((i >> S) & ((1 << S) - 1));
+}
+
+// Contiguous run of S words: widest aligned vector accesses.
+template <class W, int S> __device__ __forceinline__ void load_run(const W* src, W* v) {
+  if constexpr (S * sizeof(W) >= 16) {
+    constexpr int PER = 16 / sizeof(W);
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) {
+      uint4 u = *reinterpret_cast<const uint4*>(src + i * PER);
+      if constexpr (sizeof(W) == 8) {
+        v[2 * i] = ((uint64_t)u.y << 32) | u.x;
+        v[2 * i + 1] = ((uint64_t)u.w << 32) | u.z;
+      } else {
+        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < S; ++i) v[i] = src[i];
+  }
+}
+template <class W, int S> __device__ __forceinline__ void store_run(W* dst, const W* v) {
+  if constexpr (S * sizeof(W) >= 16) {
+    constexpr int PER = 16 / sizeof(W);
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) {
+      uint4 u;
+      if constexpr (sizeof(W) == 8) {
+        u.x = (uint32_t)v[2 * i]; u.y = (uint32_t)(v[2 * i] >> 32);
+        u.z = (uint32_t)v[2 * i + 1]; u.w = (uint32_t)(v[2 * i + 1] >> 32);
+      } else {
+        u.x = v[4 * i]; u.y = v[4 * i + 1]; u.z = v[4 * i + 2]; u.w = v[4 * i + 3];
+      }
+      *reinterpret_cast<uint4*>(dst + i * PER) = u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < S; ++i) dst[i] = v[i];
+  }
+}
+
+// Round structure: R rounds of balanced stage counts sr(r) <= LE.
+template <int LOGN, int LE> struct Rounds {
+  static constexpr int R = (LOGN + LE - 1) / LE;
+  __host__ __device__ static constexpr int sr(int r) { return LOGN / R + (r < LOGN % R ? 1 : 0); }
+  __host__ __device__ static constexpr int level(int r) {
+    int s = 0;
+    for (int i = 0; i < r; ++i) s += sr(i);
+    return s;
+  }
+};
+
+// One forward round: stages LEVEL+1 .. LEVEL+SR of Algorithm 1 on G groups of
+// 2^SR words.  Group q holds positions blk*B + h*D + c[q] (h < 2^SR) of an
+// N-point transform; stage i = LEVEL+1+j uses twiddle zeta_i^k = omega^{2^{i-1} k}
+// with k = (h mod half)*D + c, read from the table omega^e, e < N/2.
+template <class W, int LOGN, int SR, int LEVEL, int G>
+__device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, W p, W p2) {
+  constexpr int S = 1 << SR;
+  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
+#pragma unroll
+  for (int j = 0; j < SR; ++j) {
+    const int half = S >> (j + 1);
+    const bool w1 = (LEVEL + j + 1 == LOGN);  // last stage: m = 1, every twiddle is 1
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+#pragma unroll
+      for (int hh = 0; hh < half; ++hh) {
+        W w = 1, wp = 0;
+        if (!w1) ldtw<W>(tw, (uint32_t)(hh * D + c[q]) << (LEVEL + j), w, wp);
+#pragma unroll
+        for (int b = 0; b < (1 << j); ++b) {
+          const int h = b * 2 * half + hh;
+          if (w1) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], p2);
+          else bfly_alg3<W>(v[q * S + h], v[q * S + h + half], w, wp, p, p2);
+        }
+      }
+    }
+  }
+}
+
+// One inverse round: the same stages run backwards, Algorithm 4 with
+// twiddle omega^{-2^{i-1} k} from the inverse table.
+template <class W, int LOGN, int SR, int LEVEL, int G>
+__device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, W p, W p2) {
+  constexpr int S = 1 << SR;
+  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
+#pragma unroll
+  for (int j = SR - 1; j >= 0; --j) {
+    const int half = S >> (j + 1);
+    const bool w1 = (LEVEL + j + 1 == LOGN);
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+#pragma unroll
+      for (int hh = 0; hh < half; ++hh) {
+        W w = 1, wp = 0;
+        if (!w1) ldtw<W>(twi, (uint32_t)(hh * D + c[q]) << (LEVEL + j), w, wp);
+#pragma unroll
+        for (int b = 0; b < (1 << j); ++b) {
+          const int h = b * 2 * half + hh;
+          if (w1) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], p2);
+          else bfly_alg4<W>(v[q * S + h], v[q * S + h + half], w, wp, p, p2);
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- contiguous single-pass kernel
+// K transforms of N = 2^LOGN words per CTA iteration; T = N / 2^LE threads each.
+// GATHER (config C5 row pass): the input row is the concatenation of 2^log_world
+// column blocks of the all-to-all receive buffer (see ntt_fourstep_rows).
+template <int LOGN, int LE> struct ContigShape {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int E = 1 << LE;
+  static constexpr int T = N / E;
+  static constexpr int K = T >= 256 ? 1 : 256 / T;
+  static constexpr int THREADS = K * T;
+  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
+  using RC = Rounds<LOGN, LE>;
+  static constexpr int R = RC::R;
+};
+
+struct GatherArgs {
+  const void* in;             // recv buffer (GATHER) or nullptr
+  uint32_t log_w;             // log2(N2/G): width of one received block
+  uint32_t log_rows_local;    // log2(N1/G): rows per block
+};
+
+template <class W, int LOGN, int LE, bool INV, bool GATHER, int r>
+__device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* __restrict__ gin, size_t row,
+                                             const GatherArgs& ga, W* sb, int t, bool active,
+                                             const TwPair<W>* __restrict__ tw, W p, W p2, bool norm) {
+  using Sh = ContigShape<LOGN, LE>;
+  using RC = typename Sh::RC;
+  constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
+  constexpr int S = 1 << SR, G = Sh::E >> SR;
+  constexpr int D = Sh::N >> (LEVEL + SR), B = Sh::N >> LEVEL;
+  int c[G], blk[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = t + Sh::T * q;
+    blk[q] = g / D;
+    c[q] = g % D;
+  }
+  constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
+  constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
+  // ---- load
+  if constexpr (first) {
+    if constexpr (!INV) {  // natural order, strided per thread, coalesced across lanes
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int h = 0; h < S; ++h) {
+          const int i = h * D + c[q];
+          W val = 0;
+          if (active) {
+            if constexpr (GATHER) {
+              const int hb = i >> ga.log_w, off = i & ((1 << ga.log_w) - 1);
+              val = gin[(((size_t)hb << ga.log_rows_local) + row) << ga.log_w | off];
+            } else {
+              val = xb[i];
+            }
+          }
+          v[q * S + h] = val;
+        }
+    } else {  // bit-reversed input, contiguous runs
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (active) load_run<W, S>(xb + blk[q] * S, v + q * S);
+        else
+#pragma unroll
+          for (int h = 0; h < S; ++h) v[q * S + h] = 0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) v[q * S + h] = sb[swz<W>(blk[q] * B + h * D + c[q])];
+  }
+  // ---- compute
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  else dit_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  // ---- store
+  if constexpr (last) {
+    if (norm) {
+#pragma unroll
+      for (int i = 0; i < Sh::E; ++i) v[i] = INV ? norm4<W>(v[i], p, p2) : norm2<W>(v[i], p);
+    }
+    if (active) {
+      if constexpr (!INV) {
+#pragma unroll
+        for (int q = 0; q < G; ++q) store_run<W, S>(xb + blk[q] * S, v + q * S);
+      } else {
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; ++h) xb[h * D + c[q]] = v[q * S + h];
+      }
+    }
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) sb[swz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
+    __syncthreads();
+    constexpr int nr = INV ? r - 1 : r + 1;
+    contig_round<W, LOGN, LE, INV, GATHER, nr>(v, xb, gin, row, ga, sb, t, active, tw, p, p2, norm);
+  }
+}
+
+template <class W, int LOGN, int LE, bool INV, bool GATHER>
+__global__ void __launch_bounds__(ContigShape<LOGN, LE>::THREADS, ContigShape<LOGN, LE>::MINB)
+    k_contig(W* __restrict__ x, size_t batch, const TwPair<W>* __restrict__ tw, W p, int norm, GatherArgs ga) {
+  using Sh = ContigShape<LOGN, LE>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* sm = reinterpret_cast<W*>(smem_raw);
+  const int slot = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+  const W p2 = 2 * p;
+  W v[Sh::E];
+  for (size_t b0 = (size_t)blockIdx.x * Sh::K; b0 < batch; b0 += (size_t)gridDim.x * Sh::K) {
+    const size_t b = b0 + slot;
+    const bool active = b < batch;
+    W* xb = x + b * Sh::N;
+    constexpr int r0 = INV ? Sh::R - 1 : 0;
+    contig_round<W, LOGN, LE, INV, GATHER, r0>(v, xb, reinterpret_cast<const W*>(ga.in), b, ga, sm + slot * Sh::N, t,
+                                               active, tw, p, p2, norm != 0);
+  }
+}
+
+// ----------------------------------------------------------------- four-step column pass
+// Tile = N rows x C columns (C*sizeof(W) = 128 bytes), threads (t, cc) with cc
+// fastest, so every global access is a full 128-byte row segment and every smem
+// access of a (half-)warp hits one 128-byte smem row: conflict-free, no swizzle.
+template <class W> struct ColsC { static constexpr int C = 128 / sizeof(W); };
+
+template <class W, int LOGN, int LE> struct ColsShape {
+  static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E, C = ColsC<W>::C, THREADS = T * C;
+  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
+  using RC = Rounds<LOGN, LE>;
+  static constexpr int R = RC::R;
+};
+
+template <class W>
+__device__ __forceinline__ W fourstep_twiddle(W val, uint32_t e, const ColsParams& prm, const TwPair<W>* __restrict__ fa,
+                                              const TwPair<W>* __restrict__ fb, W p) {
+  W w, wp;
+  if (prm.H == 0) {
+    ldtw<W>(fa, e, w, wp);
+    return shoup_mul<W>(val, w, wp, p);
+  }
+  ldtw<W>(fb, e & ((1u << prm.H) - 1), w, wp);
+  val = shoup_mul<W>(val, w, wp, p);
+  ldtw<W>(fa, e >> prm.H, w, wp);
+  return shoup_mul<W>(val, w, wp, p);
+}
+
+template <class W, int LOGN, int LE, bool INV, int r>
+__device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int t, int cc, uint32_t cglob,
+                                           const ColsParams& prm, const TwPair<W>* __restrict__ tw,
+                                           const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p,
+                                           W p2) {
+  using Sh = ColsShape<W, LOGN, LE>;
+  using RC = typename Sh::RC;
+  constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
+  constexpr int S = 1 << SR, G = Sh::E >> SR;
+  constexpr int D = Sh::N >> (LEVEL + SR), B = Sh::N >> LEVEL;
+  constexpr int C = Sh::C;
+  const uint32_t logS = prm.log_S;
+  int c[G], blk[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = t + Sh::T * q;
+    blk[q] = g / D;
+    c[q] = g % D;
+  }
+  constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
+  constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
+  if constexpr (first) {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) {
+        const int row = blk[q] * B + h * D + c[q];
+        W val = xb[((size_t)row << logS) + cc];
+        if constexpr (INV) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
+          if (prm.twiddle) {
+            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+            const uint32_t e = ((cglob * rv) << prm.log_tw_mul);
+            const uint32_t einv = (uint32_t)((((uint64_t)1 << prm.ell) - e) & (((uint64_t)1 << prm.ell) - 1));
+            val = fourstep_twiddle<W>(val, einv, prm, fa, fb, p);
+          }
+        }
+        v[q * S + h] = val;
+      }
+  } else {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) v[q * S + h] = sm[(blk[q] * B + h * D + c[q]) * C + cc];
+  }
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  else dit_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  if constexpr (last) {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) {
+        const int row = blk[q] * B + h * D + c[q];
+        W val = v[q * S + h];
+        if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
+          if (prm.twiddle) {
+            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+            val = fourstep_twiddle<W>(val, (cglob * rv) << prm.log_tw_mul, prm, fa, fb, p);
+          }
+          if (prm.normalize) val = norm2<W>(val, p);
+        } else {
+          if (prm.normalize) val = norm4<W>(val, p, p2);
+        }
+        xb[((size_t)row << logS) + cc] = val;
+      }
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int h = 0; h < S; ++h) sm[(blk[q] * B + h * D + c[q]) * C + cc] = v[q * S + h];
+    __syncthreads();
+    constexpr int nr = INV ? r - 1 : r + 1;
+    cols_round<W, LOGN, LE, INV, nr>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, p, p2);
+  }
+}
+
+template <class W, int LOGN, int LE, bool INV>
+__global__ void __launch_bounds__(ColsShape<W, LOGN, LE>::THREADS, ColsShape<W, LOGN, LE>::MINB)
+    k_cols(W* __restrict__ x, ColsParams prm, const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
+           const TwPair<W>* __restrict__ fb, W p) {
+  using Sh = ColsShape<W, LOGN, LE>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* sm = reinterpret_cast<W*>(smem_raw);
+  const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
+  const W p2 = 2 * p;
+  W v[Sh::E];
+  const uint64_t cg_mask = ((uint64_t)1 << prm.log_colgroups) - 1;
+  for (uint64_t tile = blockIdx.x; tile < prm.n_tiles; tile += gridDim.x) {
+    const uint64_t bq = tile >> prm.log_colgroups, cg = tile & cg_mask;
+    // block bq spans N*S words; this tile covers columns [cg*C, cg*C + C)
+    W* xb = x + (bq << (LOGN + prm.log_S)) + cg * Sh::C;
+    uint32_t cloc = (uint32_t)(cg * Sh::C + cc);
+    uint32_t cglob = cloc;
+    if (prm.shard) {  // local flat column -> global column of the N1 x N2 matrix
+      const uint32_t rb = cloc >> prm.log_local_w, cl = cloc & ((1u << prm.log_local_w) - 1);
+      cglob = (rb << prm.log_n2) | (prm.col0 + cl);
+    }
+    constexpr int r0 = INV ? Sh::R - 1 : 0;
+    cols_round<W, LOGN, LE, INV, r0>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, p, p2);
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------- pointwise, normalise
+// c = a b L^{-1} mod p: Montgomery REDC in the Alg. 5 pattern gives
+// a b beta^{-1} in (0,2p); a Shoup multiply by K = beta L^{-1} mod p (or beta mod p
+// without scaling) restores the scale; then normalise.
+template <class W>
+__global__ void k_pointwise(W* __restrict__ c, const W* __restrict__ a, const W* __restrict__ b, size_t n, W p, W J,
+                            W K, W Kp) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    W r = mont_redc_mul<W>(a[i], b[i], J, p);
+    r = shoup_mul<W>(r, K, Kp, p);
+    c[i] = norm2<W>(r, p);
+  }
+}
+
+template <class W> __global__ void k_normalize(W* __restrict__ x, size_t n, W p, int from4p) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const W p2 = 2 * p;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    x[i] = from4p ? norm4<W>(x[i], p, p2) : norm2<W>(x[i], p);
+}
+
+template <class W>
+__global__ void k_debug_bfly(int alg, const W* __restrict__ Wv, const W* __restrict__ Wpv, W* __restrict__ X,
+                             W* __restrict__ Y, size_t n, W p, W J) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  W x = X[i], y = Y[i];
+  const W p2 = 2 * p;
+  switch (alg) {
+    case 2: bfly_alg2<W>(x, y, Wv[i], Wpv[i], p); break;
+    case 3: bfly_alg3<W>(x, y, Wv[i], Wpv[i], p, p2); break;
+    case 31: bfly_alg3_w1<W>(x, y, p2); break;
+    case 4: bfly_alg4<W>(x, y, Wv[i], Wpv[i], p, p2); break;
+    case 41: bfly_alg4_w1<W>(x, y, p2); break;
+    case 5: bfly_alg5<W>(x, y, Wpv[i], J, p, p2); break;
+    default: break;
+  }
+  X[i] = x;
+  Y[i] = y;
+}
+
+// ----------------------------------------------------------------- ALU calibration
+// Register-only Algorithm 3 loop: 8 independent butterfly chains per thread.
+template <class W>
+__global__ void __launch_bounds__(256) k_calib(W* sink, W p, W w, W wp, unsigned iters) {
+  constexpr int CH = 8;
+  W x[CH], y[CH];
+  const W p2 = 2 * p;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    x[c] = (W)(threadIdx.x * 7 + c) % p;
+    y[c] = (W)(threadIdx.x * 13 + 3 * c) % p;
+  }
+  for (unsigned i = 0; i < iters; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) bfly_alg3<W>(x[c], y[c], w, wp, p, p2);
+  W s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s ^= x[c] ^ y[c];
+  if (s == (W)0x12345678u) sink[0] = s;
+}
+
+// ----------------------------------------------------------------- launch plumbing
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <class KernelT> static int occupancy(KernelT k, int threads, size_t smem) {
+  int blocks = 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, threads, smem);
+  return blocks > 0 ? blocks : 1;
+}
+
+// per-(W, LOGN) elements-per-thread choice
+template <class W, int LOGN> struct ContigLE {
+  static constexpr int value = sizeof(W) == 8 ? (LOGN <= 4 ? LOGN : (LOGN <= 13 ? 4 : 5))
+                                              : (LOGN <= 5 ? LOGN : 5);
+};
+
+template <class W, int LOGN, bool INV, bool GATHER>
+static cudaError_t run_contig(void* x, size_t batch, const void* tw, uint64_t p, bool norm, GatherArgs ga,
+                              cudaStream_t s) {
+  constexpr int LE = ContigLE<W, LOGN>::value;
+  using Sh = ContigShape<LOGN, LE>;
+  const size_t smem = Sh::R > 1 ? (size_t)Sh::K * Sh::N * sizeof(W) : 0;
+  auto kern = k_contig<W, LOGN, LE, INV, GATHER>;
+  static int occ = 0;
+  if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
+  const size_t iters = (batch + Sh::K - 1) / Sh::K;
+  const size_t maxg = (size_t)occ * num_sms();
+  const unsigned grid = (unsigned)(iters < maxg ? iters : maxg);
+  if (!grid) return cudaSuccess;
+  kern<<<grid, Sh::THREADS, smem, s>>>(reinterpret_cast<W*>(x), batch, reinterpret_cast<const TwPair<W>*>(tw),
+                                       (W)p, norm ? 1 : 0, ga);
+  return cudaGetLastError();
+}
+
+template <class W, int LOGN> struct ColsLE {
+  static constexpr int value = sizeof(W) == 8 ? 4 : (LOGN < 5 ? LOGN : 5);
+};
+
+template <class W, int LOGN, bool INV>
+static cudaError_t run_cols(void* x, const ColsParams& prm, const DevTables& t, uint64_t p, cudaStream_t s) {
+  constexpr int LE = ColsLE<W, LOGN>::value;
+  using Sh = ColsShape<W, LOGN, LE>;
+  const size_t smem = (size_t)Sh::N * Sh::C * sizeof(W);
+  auto kern = k_cols<W, LOGN, LE, INV>;
+  static int occ = 0;
+  if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
+  const uint64_t maxg = (uint64_t)occ * num_sms();
+  const unsigned grid = (unsigned)(prm.n_tiles < maxg ? prm.n_tiles : maxg);
+  if (!grid) return cudaSuccess;
+  kern<<<grid, Sh::THREADS, smem, s>>>(reinterpret_cast<W*>(x), prm,
+                                       reinterpret_cast<const TwPair<W>*>(INV ? t.sub_inv : t.sub_fwd),
+                                       reinterpret_cast<const TwPair<W>*>(t.fa),
+                                       reinterpret_cast<const TwPair<W>*>(t.fb), (W)p);
+  return cudaGetLastError();
+}
+
+// compile-time dispatch over LOGN
+template <class W, bool INV, bool GATHER, int LO, int HI>
+static cudaError_t contig_dispatch(int logn, void* x, size_t batch, const void* tw, uint64_t p, bool norm,
+                                   GatherArgs ga, cudaStream_t s) {
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (logn == LO) return run_contig<W, LO, INV, GATHER>(x, batch, tw, p, norm, ga, s);
+    return contig_dispatch<W, INV, GATHER, LO + 1, HI>(logn, x, batch, tw, p, norm, ga, s);
+  }
+}
+
+template <class W, bool INV, int LO, int HI>
+static cudaError_t cols_dispatch(int logn, void* x, const ColsParams& prm, const DevTables& t, uint64_t p,
+                                 cudaStream_t s) {
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (logn == LO) return run_cols<W, LO, INV>(x, prm, t, p, s);
+    return cols_dispatch<W, INV, LO + 1, HI>(logn, x, prm, t, p, s);
+  }
+}
+
+cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch, const void* tw,
+                          uint64_t p, cudaStream_t s) {
+  GatherArgs ga{nullptr, 0, 0};
+  if (wbytes == 8) {
+    return inverse ? contig_dispatch<uint64_t, true, false, 1, kContigMaxLog64>(logn, x, batch, tw, p, normalize, ga, s)
+                   : contig_dispatch<uint64_t, false, false, 1, kContigMaxLog64>(logn, x, batch, tw, p, normalize, ga, s);
+  }
+  return inverse ? contig_dispatch<uint32_t, true, false, 1, kContigMaxLog32>(logn, x, batch, tw, p, normalize, ga, s)
+                 : contig_dispatch<uint32_t, false, false, 1, kContigMaxLog32>(logn, x, batch, tw, p, normalize, ga, s);
+}
+
+cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
+                               uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s) {
+  GatherArgs ga{recv, (uint32_t)logn2 - log_world, log_rows_local};
+  const size_t rows = (size_t)1 << log_rows_local;
+  if (wbytes == 8)
+    return contig_dispatch<uint64_t, false, true, 5, kContigMaxLog64>(logn2, out, rows, tw, p, true, ga, s);
+  return contig_dispatch<uint32_t, false, true, 5, kContigMaxLog32>(logn2, out, rows, tw, p, true, ga, s);
+}
+
+cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
+                        uint64_t p, cudaStream_t s) {
+  if (wbytes == 8)
+    return inverse ? cols_dispatch<uint64_t, true, kColsMinLog, kColsMaxLog64>(logn, x, prm, t, p, s)
+                   : cols_dispatch<uint64_t, false, kColsMinLog, kColsMaxLog64>(logn, x, prm, t, p, s);
+  return inverse ? cols_dispatch<uint32_t, true, kColsMinLog, kColsMaxLog32>(logn, x, prm, t, p, s)
+                 : cols_dispatch<uint32_t, false, kColsMinLog, kColsMaxLog32>(logn, x, prm, t, p, s);
+}
+
+static unsigned elementwise_grid(size_t n, int threads) {
+  size_t g = (n + threads - 1) / threads;
+  size_t cap = (size_t)num_sms() * 16;
+  return (unsigned)(g < cap ? (g ? g : 1) : cap);
+}
+
+cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, size_t n, uint64_t p, uint64_t J,
+                             uint64_t K, uint64_t Kp, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const int th = 256;
+  if (wbytes == 8)
+    k_pointwise<uint64_t><<<elementwise_grid(n, th), th, 0, s>>>((uint64_t*)c, (const uint64_t*)a, (const uint64_t*)b,
+                                                                   n, p, J, K, Kp);
+  else
+    k_pointwise<uint32_t><<<elementwise_grid(n, th), th, 0, s>>>((uint32_t*)c, (const uint32_t*)a, (const uint32_t*)b,
+                                                                   n, (uint32_t)p, (uint32_t)J, (uint32_t)K,
+                                                                   (uint32_t)Kp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(int wbytes, void* x, size_t n, uint64_t p, int from4p, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const int th = 256;
+  if (wbytes == 8) k_normalize<uint64_t><<<elementwise_grid(n, th), th, 0, s>>>((uint64_t*)x, n, p, from4p);
+  else k_normalize<uint32_t><<<elementwise_grid(n, th), th, 0, s>>>((uint32_t*)x, n, (uint32_t)p, from4p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_calib(int wbytes, uint64_t p, uint64_t w, uint64_t wp, unsigned iters, void* sink,
+                         uint64_t* n_bfly, cudaStream_t s) {
+  const unsigned grid = (unsigned)num_sms() * 8, th = 256;
+  *n_bfly = (uint64_t)grid * th * 8 * iters;
+  if (wbytes == 8) k_calib<uint64_t><<<grid, th, 0, s>>>((uint64_t*)sink, p, w, wp, iters);
+  else k_calib<uint32_t><<<grid, th, 0, s>>>((uint32_t*)sink, (uint32_t)p, (uint32_t)w, (uint32_t)wp, iters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_bfly(int wbytes, int alg, const void* W, const void* Wp, void* X, void* Y, size_t n,
+                              uint64_t p, uint64_t J, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const int th = 256;
+  const unsigned grid = (unsigned)((n + th - 1) / th);
+  if (wbytes == 8)
+    k_debug_bfly<uint64_t><<<grid, th, 0, s>>>(alg, (const uint64_t*)W, (const uint64_t*)Wp, (uint64_t*)X,
+                                                (uint64_t*)Y, n, p, J);
+  else
+    k_debug_bfly<uint32_t><<<grid, th, 0, s>>>(alg, (const uint32_t*)W, (const uint32_t*)Wp, (uint32_t*)X,
+                                                (uint32_t*)Y, n, (uint32_t)p, (uint32_t)J);
+  return cudaGetLastError();
+}
+
+}  // namespace nttb

@@ -1,0 +1,623 @@
+// plan.cu -- host side of the C ABI (include/ntt_b200.h): plan validation,
+// twiddle precompute, the pass schedule, and the entry points.
+//
+// Twiddle precompute ("W and W' ... can be precomputed and reused"):
+// W_e = omega^e by repeated multiplication, W'_e = floor(W_e beta / p) by a
+// 128-bit division, so W' p <= W beta < (W'+1) p exactly (the bound used in the
+// proof of Theorem 1).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/ntt_b200.h"
+#include "internal.h"
+
+using u128 = unsigned __int128;
+
+namespace {
+
+thread_local unsigned t_launches = 0;
+thread_local char t_cuda_err[256] = "";
+
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)((u128)a * b % p); }
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  b %= p;
+  for (; e; e >>= 1, b = mulmod(b, b, p))
+    if (e & 1) r = mulmod(r, b, p);
+  return r;
+}
+
+// Deterministic Miller-Rabin for 64-bit n (the first 12 prime bases suffice).
+bool is_prime_u64(uint64_t n) {
+  if (n < 2) return false;
+  static const uint64_t small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (uint64_t q : small) {
+    if (n % q == 0) return n == q;
+  }
+  uint64_t d = n - 1;
+  int s = 0;
+  while (!(d & 1)) d >>= 1, ++s;
+  for (uint64_t a : small) {
+    uint64_t x = powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < s; ++i) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
+// Table of (root^e, floor(root^e beta / p)) for e < count, interleaved pairs of
+// the plan's word width.
+std::vector<uint8_t> make_table(uint64_t p, uint64_t root, uint64_t count, unsigned bits) {
+  const size_t wb = bits / 8;
+  std::vector<uint8_t> out(count * 2 * wb);
+  uint64_t w = 1 % p;
+  for (uint64_t e = 0; e < count; ++e) {
+    const uint64_t wp = (uint64_t)(((u128)w << bits) / p);
+    if (wb == 8) {
+      memcpy(&out[(2 * e) * 8], &w, 8);
+      memcpy(&out[(2 * e + 1) * 8], &wp, 8);
+    } else {
+      const uint32_t w32 = (uint32_t)w, wp32 = (uint32_t)wp;
+      memcpy(&out[(2 * e) * 4], &w32, 4);
+      memcpy(&out[(2 * e + 1) * 4], &wp32, 4);
+    }
+    w = mulmod(w, root, p);
+  }
+  return out;
+}
+
+}  // namespace
+
+struct ntt_plan_s {
+  int device = 0;
+  uint64_t p = 0, omega = 0, omega_inv = 0, L_inv = 0, J = 0;
+  unsigned ell = 0, bits = 0, wbytes = 0;
+  // schedule: log2 sub-lengths of the passes, outermost first
+  std::vector<unsigned> passes;
+  // device tables
+  void* tw_fwd = nullptr;  // single pass: omega^e, e < L/2
+  void* tw_inv = nullptr;  // single pass: omega^{-e}
+  std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables
+  void* fa = nullptr;                   // four-step table (direct when H == 0)
+  void* fb = nullptr;
+  unsigned H = 0;
+  std::vector<void*> owned;
+  // lazily built tables for the distributed four-step entry points (guarded by mu)
+  std::mutex mu;
+  std::map<unsigned, void*> extra_sub;  // log2 N -> omega_N^e table
+  // host-buffer executor (ntt_execute_host): pipeline streams and events
+  static constexpr int kSlots = 3;
+  cudaStream_t pipe[kSlots] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_done[kSlots] = {nullptr, nullptr, nullptr};
+  cudaEvent_t start_ev = nullptr;
+  // pointwise constants: K = beta mod p (plain) / beta L^{-1} mod p (scaled) and K'
+  uint64_t K_plain = 0, Kp_plain = 0, K_scale = 0, Kp_scale = 0;
+};
+
+namespace {
+
+ntt_status cuda_fail(cudaError_t e) {
+  snprintf(t_cuda_err, sizeof t_cuda_err, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return NTT_ERR_CUDA;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+ntt_status upload(ntt_plan_s* pl, const std::vector<uint8_t>& host, void** out) {
+  void* d = nullptr;
+  const size_t n = host.empty() ? 16 : host.size();
+  cudaError_t e = cudaMalloc(&d, n);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? NTT_ERR_NOMEM : cuda_fail(e);
+  pl->owned.push_back(d);
+  if (!host.empty()) {
+    e = cudaMemcpy(d, host.data(), host.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  *out = d;
+  return NTT_OK;
+}
+
+void free_plan(ntt_plan_s* pl) {
+  if (!pl) return;
+  {
+    DeviceGuard g(pl->device);
+    for (void* d : pl->owned) cudaFree(d);
+    for (int i = 0; i < ntt_plan_s::kSlots; ++i) {
+      if (pl->pipe[i]) cudaStreamDestroy(pl->pipe[i]);
+      if (pl->pipe_done[i]) cudaEventDestroy(pl->pipe_done[i]);
+    }
+    if (pl->start_ev) cudaEventDestroy(pl->start_ev);
+  }
+  delete pl;
+}
+
+// Pass schedule: one on-chip pass when the
+// transform fits; otherwise column passes of <= kColsMax stages followed by one
+// contiguous row pass of <= kContigMax stages, stage counts balanced.
+std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
+  const unsigned cmax = wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
+  const unsigned colmax = wbytes == 8 ? nttb::kColsMaxLog64 : nttb::kColsMaxLog32;
+  if (ell <= cmax) return {ell};
+  for (unsigned np = 2;; ++np) {
+    const unsigned col = std::min(colmax, ell / np);
+    const unsigned last = ell - col * (np - 1);
+    if (last <= cmax) {
+      std::vector<unsigned> s(np, col);
+      s[np - 1] = last;
+      return s;
+    }
+  }
+}
+
+// Table omega_N^e (e < N/2) for N = 2^logn, built once per plan (distributed entry points).
+ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out) {
+  std::lock_guard<std::mutex> lk(pl->mu);
+  auto it = pl->extra_sub.find(logn);
+  if (it != pl->extra_sub.end()) { *out = it->second; return NTT_OK; }
+  const uint64_t L = (uint64_t)1 << pl->ell, Nn = (uint64_t)1 << logn;
+  void* d = nullptr;
+  ntt_status st = upload(pl, make_table(pl->p, powmod(pl->omega, L / Nn, pl->p), Nn / 2, pl->bits), &d);
+  if (st != NTT_OK) return st;
+  pl->extra_sub[logn] = d;
+  *out = d;
+  return NTT_OK;
+}
+
+// Four-step twiddles omega_L^e, e < L: direct table for ell <= 16, else factored
+// omega^e = omega^{(e >> H) << H} * omega^{e & (2^H - 1)} (two Shoup multiplies).
+ntt_status build_fourstep_tables(ntt_plan_s* pl) {
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  ntt_status st;
+  if (pl->ell <= 16) {
+    pl->H = 0;
+    st = upload(pl, make_table(pl->p, pl->omega, L, pl->bits), &pl->fa);
+    pl->fb = pl->fa;
+  } else {
+    pl->H = (pl->ell + 1) / 2;
+    st = upload(pl, make_table(pl->p, powmod(pl->omega, (uint64_t)1 << pl->H, pl->p), L >> pl->H, pl->bits), &pl->fa);
+    if (st == NTT_OK) st = upload(pl, make_table(pl->p, pl->omega, (uint64_t)1 << pl->H, pl->bits), &pl->fb);
+  }
+  return st;
+}
+
+ntt_status ensure_fourstep_tables(ntt_plan_s* pl) {
+  std::lock_guard<std::mutex> lk(pl->mu);
+  if (pl->fa) return NTT_OK;
+  return build_fourstep_tables(pl);
+}
+
+}  // namespace
+
+extern "C" {
+
+unsigned ntt_abi_version(void) { return 1; }
+
+const char* ntt_status_str(ntt_status s) {
+  switch (s) {
+    case NTT_OK: return "ok";
+    case NTT_ERR_ARG: return "invalid argument";
+    case NTT_ERR_MODULUS: return "modulus must be an odd prime p < beta/4";
+    case NTT_ERR_ROOT: return "omega is not a primitive 2^ell-th root of unity mod p";
+    case NTT_ERR_LENGTH: return "2^ell must divide p-1 and ell <= 28";
+    case NTT_ERR_WORD: return "log2_beta must be 32 or 64";
+    case NTT_ERR_CUDA: return "CUDA error";
+    case NTT_ERR_NOMEM: return "out of memory";
+    case NTT_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* ntt_last_cuda_error(void) { return t_cuda_err; }
+unsigned ntt_last_launch_count(void) { return t_launches; }
+
+ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta, int device) {
+  if (!out) return NTT_ERR_ARG;
+  *out = nullptr;
+  if (log2_beta != 32 && log2_beta != 64) return NTT_ERR_WORD;
+  // P:114 / P:146: p < beta/4; p odd prime ("word-sized prime", Alg. 5 "p odd")
+  const u128 beta = (u128)1 << log2_beta;
+  if (p < 3 || !(p & 1) || (u128)p * 4 >= beta || !is_prime_u64(p)) return NTT_ERR_MODULUS;
+  if (ell > 28) return NTT_ERR_LENGTH;
+  const uint64_t L = (uint64_t)1 << ell;
+  if ((p - 1) % L != 0) return NTT_ERR_LENGTH;  // p = 1 mod L
+  if (omega >= p) return NTT_ERR_ROOT;
+  if (ell == 0) {
+    if (omega != 1) return NTT_ERR_ROOT;
+  } else if (powmod(omega, L / 2, p) != p - 1) {
+    return NTT_ERR_ROOT;  // primitive L-th root <=> omega^(L/2) = -1
+  }
+  ntt_plan_s* pl = new (std::nothrow) ntt_plan_s();
+  if (!pl) return NTT_ERR_NOMEM;
+  pl->device = device;
+  pl->p = p;
+  pl->omega = omega;
+  pl->omega_inv = powmod(omega, p - 2, p);
+  pl->L_inv = powmod(L % p, p - 2, p);
+  pl->ell = ell;
+  pl->bits = log2_beta;
+  pl->wbytes = log2_beta / 8;
+  {
+    // J = p^{-1} mod beta by Newton iteration
+    uint64_t j = p;  // correct to 3 bits for odd p
+    for (int i = 0; i < 6; ++i) j *= 2 - p * j;
+    pl->J = log2_beta == 32 ? (uint64_t)(uint32_t)j : j;
+  }
+  {
+    const uint64_t bmodp = (uint64_t)(beta % p);
+    pl->K_plain = bmodp;
+    pl->Kp_plain = (uint64_t)(((u128)bmodp << log2_beta) / p);
+    pl->K_scale = mulmod(bmodp, pl->L_inv, p);
+    pl->Kp_scale = (uint64_t)(((u128)pl->K_scale << log2_beta) / p);
+  }
+  pl->passes = make_schedule(ell, pl->wbytes);
+  DeviceGuard g(device);
+  if (!g.ok) { delete pl; return cuda_fail(cudaGetLastError()); }
+  ntt_status st = NTT_OK;
+  const unsigned bits = log2_beta;
+  if (pl->passes.size() == 1) {
+    const uint64_t half = L / 2;
+    if ((st = upload(pl, make_table(p, omega, half, bits), &pl->tw_fwd)) != NTT_OK ||
+        (st = upload(pl, make_table(p, pl->omega_inv, half, bits), &pl->tw_inv)) != NTT_OK) {
+      free_plan(pl);
+      return st;
+    }
+  } else {
+    for (unsigned n : pl->passes) {
+      const uint64_t Nn = (uint64_t)1 << n;
+      const uint64_t rootN = powmod(omega, L / Nn, p), rootNi = powmod(pl->omega_inv, L / Nn, p);
+      void *f = nullptr, *i = nullptr;
+      if ((st = upload(pl, make_table(p, rootN, Nn / 2, bits), &f)) != NTT_OK ||
+          (st = upload(pl, make_table(p, rootNi, Nn / 2, bits), &i)) != NTT_OK) {
+        free_plan(pl);
+        return st;
+      }
+      pl->sub_fwd.push_back(f);
+      pl->sub_inv.push_back(i);
+    }
+    st = build_fourstep_tables(pl);
+    if (st != NTT_OK) { free_plan(pl); return st; }
+  }
+  *out = pl;
+  return NTT_OK;
+}
+
+ntt_status ntt_plan_destroy(ntt_plan_t plan) {
+  if (!plan) return NTT_ERR_ARG;
+  free_plan(plan);
+  return NTT_OK;
+}
+
+ntt_status ntt_plan_info(ntt_plan_t pl, ntt_plan_info_t* out) {
+  if (!pl || !out) return NTT_ERR_ARG;
+  memset(out, 0, sizeof *out);
+  out->p = pl->p;
+  out->omega = pl->omega;
+  out->omega_inv = pl->omega_inv;
+  out->L_inv = pl->L_inv;
+  out->ell = pl->ell;
+  out->log2_beta = pl->bits;
+  out->word_bytes = pl->wbytes;
+  out->n_passes = (unsigned)pl->passes.size();
+  for (size_t i = 0; i < pl->passes.size() && i < 4; ++i) out->pass_log2[i] = pl->passes[i];
+  out->device = pl->device;
+  return NTT_OK;
+}
+
+ntt_status ntt_plan_twiddles(ntt_plan_t pl, void* host_W, void* host_Wp) {
+  if (!pl || !host_W || !host_Wp) return NTT_ERR_ARG;
+  if (pl->ell > 20) return NTT_ERR_UNSUPPORTED;
+  const uint64_t half = ((uint64_t)1 << pl->ell) / 2;
+  std::vector<uint8_t> t;
+  if (pl->tw_fwd) {  // the device table the kernels read
+    DeviceGuard g(pl->device);
+    t.resize(half * 2 * pl->wbytes);
+    if (half) {
+      cudaError_t e = cudaMemcpy(t.data(), pl->tw_fwd, t.size(), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+  } else {
+    t = make_table(pl->p, pl->omega, half, pl->bits);
+  }
+  const size_t wb = pl->wbytes;
+  for (uint64_t e = 0; e < half; ++e) {
+    memcpy((uint8_t*)host_W + e * wb, &t[(2 * e) * wb], wb);
+    memcpy((uint8_t*)host_Wp + e * wb, &t[(2 * e + 1) * wb], wb);
+  }
+  return NTT_OK;
+}
+
+static bool aligned16(const void* x) { return ((uintptr_t)x & 15) == 0; }
+
+static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
+  t_launches = 0;
+  if (!pl || (!x && batch) || (x && !aligned16(x))) return NTT_ERR_ARG;
+  if (!batch) return NTT_OK;
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  if (batch > (SIZE_MAX / pl->wbytes) / L) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  if (!g.ok) return cuda_fail(cudaGetLastError());
+  cudaError_t e = cudaSuccess;
+  const unsigned np = (unsigned)pl->passes.size();
+  if (pl->ell == 0) {  // identity; only the normalisation remains
+    e = nttb::launch_normalize(pl->wbytes, x, batch, pl->p, inverse ? 1 : 0, s);
+    ++t_launches;
+    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+  }
+  if (np == 1) {
+    e = nttb::launch_contig(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
+                            pl->p, s);
+    ++t_launches;
+    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+  }
+  // nested four-step: passes 0..np-2 are column passes, np-1 the contiguous row pass
+  const unsigned C = 128 / pl->wbytes;
+  auto cols_params = [&](unsigned j, bool normalize) {
+    nttb::ColsParams prm{};
+    unsigned outer = 0;
+    for (unsigned i = 0; i < j; ++i) outer += pl->passes[i];
+    const unsigned logB = pl->ell - outer, logN = pl->passes[j], logS = logB - logN;
+    unsigned logC = 0;
+    while ((1u << logC) < C) ++logC;
+    prm.log_S = logS;
+    prm.log_colgroups = logS - logC;
+    prm.n_tiles = ((uint64_t)batch << outer) << prm.log_colgroups;
+    prm.log_tw_mul = outer;
+    prm.ell = pl->ell;
+    prm.H = pl->H;
+    prm.twiddle = 1;
+    prm.normalize = normalize ? 1 : 0;
+    return prm;
+  };
+  if (!inverse) {
+    for (unsigned j = 0; j + 1 < np && e == cudaSuccess; ++j) {
+      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
+      e = nttb::launch_cols(pl->wbytes, (int)pl->passes[j], false, x, cols_params(j, false), t, pl->p, s);
+      ++t_launches;
+    }
+    if (e == cudaSuccess) {
+      const size_t rows = batch * (L >> pl->passes[np - 1]);
+      e = nttb::launch_contig(pl->wbytes, (int)pl->passes[np - 1], false, true, x, rows, pl->sub_fwd[np - 1], pl->p, s);
+      ++t_launches;
+    }
+  } else {
+    const size_t rows = batch * (L >> pl->passes[np - 1]);
+    e = nttb::launch_contig(pl->wbytes, (int)pl->passes[np - 1], true, false, x, rows, pl->sub_inv[np - 1], pl->p, s);
+    ++t_launches;
+    for (int j = (int)np - 2; j >= 0 && e == cudaSuccess; --j) {
+      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
+      e = nttb::launch_cols(pl->wbytes, (int)pl->passes[j], true, x, cols_params((unsigned)j, j == 0), t, pl->p, s);
+      ++t_launches;
+    }
+  }
+  (void)C;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, void* host_out, size_t batch,
+                            void* dev_buf, size_t dev_buf_bytes, ntt_stream_t stream) {
+  if (!pl || !ops || (ops & ~(NTT_OP_FORWARD | NTT_OP_INVERSE))) return NTT_ERR_ARG;
+  if (!batch) { t_launches = 0; return NTT_OK; }
+  if (!host_in || !host_out || !dev_buf || !aligned16(dev_buf)) return NTT_ERR_ARG;
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  const size_t tbytes = (size_t)L * pl->wbytes;
+  if (batch > SIZE_MAX / tbytes || dev_buf_bytes < tbytes) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  {
+    std::lock_guard<std::mutex> lk(pl->mu);
+    if (!pl->start_ev) {
+      for (int i = 0; i < ntt_plan_s::kSlots; ++i) {
+        cudaError_t e = cudaStreamCreateWithFlags(&pl->pipe[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->pipe_done[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e);
+      }
+      cudaError_t e = cudaEventCreateWithFlags(&pl->start_ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+  }
+  // chunking: up to kSlots chunks resident in dev_buf, each >= 1 transform
+  const int slots = (int)std::min<size_t>(ntt_plan_s::kSlots, dev_buf_bytes / tbytes);
+  const size_t per_slot = dev_buf_bytes / slots / tbytes;        // transforms per chunk buffer
+  const size_t want = (batch + 4 * slots - 1) / (4 * slots);      // aim for >= 4 chunks per slot
+  const size_t chunk = std::max<size_t>(1, std::min(per_slot, want));
+  cudaStream_t user = (cudaStream_t)stream;
+  cudaError_t e = cudaEventRecord(pl->start_ev, user);
+  for (int i = 0; e == cudaSuccess && i < slots; ++i) e = cudaStreamWaitEvent(pl->pipe[i], pl->start_ev, 0);
+  if (e != cudaSuccess) return cuda_fail(e);
+  unsigned launches = 0;
+  int k = 0;
+  for (size_t b0 = 0; b0 < batch; b0 += chunk, k = (k + 1) % slots) {
+    const size_t nb = std::min(chunk, batch - b0);
+    void* d = (uint8_t*)dev_buf + (size_t)k * per_slot * tbytes;
+    cudaStream_t s = pl->pipe[k];
+    e = cudaMemcpyAsync(d, (const uint8_t*)host_in + b0 * tbytes, nb * tbytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (ops & NTT_OP_FORWARD) {
+      ntt_status st = run_transform(pl, d, nb, s, false);
+      launches += t_launches;
+      if (st != NTT_OK) return st;
+    }
+    if (ops & NTT_OP_INVERSE) {
+      ntt_status st = run_transform(pl, d, nb, s, true);
+      launches += t_launches;
+      if (st != NTT_OK) return st;
+    }
+    e = cudaMemcpyAsync((uint8_t*)host_out + b0 * tbytes, d, nb * tbytes, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  for (int i = 0; e == cudaSuccess && i < slots; ++i) {
+    e = cudaEventRecord(pl->pipe_done[i], pl->pipe[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, pl->pipe_done[i], 0);
+  }
+  t_launches = launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream) {
+  return run_transform(plan, x, batch, (cudaStream_t)stream, false);
+}
+
+ntt_status ntt_inverse(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream) {
+  return run_transform(plan, x, batch, (cudaStream_t)stream, true);
+}
+
+ntt_status ntt_pointwise_mul(ntt_plan_t pl, void* c, const void* a, const void* b, size_t batch, unsigned flags,
+                             ntt_stream_t stream) {
+  t_launches = 0;
+  if (!pl || flags > NTT_SCALE_INV_L) return NTT_ERR_ARG;
+  if (!batch) return NTT_OK;
+  if (!c || !a || !b) return NTT_ERR_ARG;
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  if (batch > (SIZE_MAX / pl->wbytes) / L) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  const bool sc = flags & NTT_SCALE_INV_L;
+  cudaError_t e = nttb::launch_pointwise(pl->wbytes, c, a, b, batch * L, pl->p, pl->J, sc ? pl->K_scale : pl->K_plain,
+                                         sc ? pl->Kp_scale : pl->Kp_plain, (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, ntt_stream_t stream) {
+  if (!pl) return NTT_ERR_ARG;
+  unsigned total = 0;
+  ntt_status st = ntt_forward(pl, a, batch, stream);
+  total += t_launches;
+  if (st == NTT_OK) { st = ntt_forward(pl, b, batch, stream); total += t_launches; }
+  if (st == NTT_OK) { st = ntt_pointwise_mul(pl, a, a, b, batch, NTT_SCALE_INV_L, stream); total += t_launches; }
+  if (st == NTT_OK) { st = ntt_inverse(pl, a, batch, stream); total += t_launches; }
+  t_launches = total;
+  return st;
+}
+
+ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
+                             ntt_stream_t stream) {
+  t_launches = 0;
+  if (!pl || !x || !aligned16(x) || world == 0 || (world & (world - 1)) || rank >= world) return NTT_ERR_ARG;
+  if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
+  const unsigned ell2 = pl->ell - ell1;
+  unsigned lw = 0;
+  while ((1u << lw) < world) ++lw;
+  const unsigned C = 128 / pl->wbytes;
+  if (lw > ell1 || (ell2 < lw) || ((1u << (ell2 - lw)) < C)) return NTT_ERR_ARG;
+  const unsigned colmax = pl->wbytes == 8 ? nttb::kColsMaxLog64 : nttb::kColsMaxLog32;
+  // split the length-N1 column DFT into column passes of <= colmax stages
+  const unsigned nc = (ell1 + colmax - 1) / colmax;
+  std::vector<unsigned> cp(nc, ell1 / nc);
+  for (unsigned i = 0; i < ell1 % nc; ++i) cp[nc - 1 - i] += 1;
+  const unsigned log_wl = ell2 - lw;  // local width N2/G
+  unsigned logC = 0;
+  while ((1u << logC) < C) ++logC;
+  DeviceGuard g(pl->device);
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  cudaError_t e = cudaSuccess;
+  unsigned outer = 0;
+  for (unsigned j = 0; j < nc && e == cudaSuccess; ++j) {
+    const unsigned logN = cp[j];
+    // local block = rows of this sub-level x local width
+    const unsigned logS = (ell1 - outer - logN) + log_wl;
+    nttb::ColsParams prm{};
+    prm.log_S = logS;
+    prm.log_colgroups = logS - logC;
+    prm.n_tiles = ((uint64_t)1 << outer) << prm.log_colgroups;
+    prm.log_tw_mul = outer;
+    prm.ell = pl->ell;
+    prm.H = pl->H;
+    prm.twiddle = 1;
+    prm.normalize = 0;
+    prm.shard = 1;
+    prm.log_local_w = log_wl;
+    prm.log_n2 = ell2;
+    prm.col0 = rank << log_wl;
+    void* subf = nullptr;
+    ntt_status st = sub_table(pl, logN, &subf);
+    if (st == NTT_OK) st = ensure_fourstep_tables(pl);
+    if (st != NTT_OK) return st;
+    nttb::DevTables t{subf, subf, pl->fa, pl->fb};
+    e = nttb::launch_cols(pl->wbytes, (int)logN, false, x, prm, t, pl->p, (cudaStream_t)stream);
+    ++t_launches;
+    outer += logN;
+  }
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,
+                             ntt_stream_t stream) {
+  t_launches = 0;
+  if (!pl || !recv || !out || !aligned16(out) || world == 0 || (world & (world - 1)) || rank >= world)
+    return NTT_ERR_ARG;
+  if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
+  const unsigned ell2 = pl->ell - ell1;
+  const unsigned cmax = pl->wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
+  if (ell2 > cmax || ell2 < 5) return NTT_ERR_UNSUPPORTED;
+  unsigned lw = 0;
+  while ((1u << lw) < world) ++lw;
+  if (lw > ell1 || lw > ell2) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  const uint64_t N2 = (uint64_t)1 << ell2;
+  void* subf = nullptr;
+  ntt_status st = sub_table(pl, ell2, &subf);
+  if (st != NTT_OK) return st;
+  cudaError_t e = nttb::launch_rows_gather(pl->wbytes, (int)ell2, out, recv, ell1 - lw, lw, subf, pl->p,
+                                           (cudaStream_t)stream);
+  ++t_launches;
+  (void)rank;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_synth_uniform(void* x, size_t count, unsigned word_bytes, uint64_t seed, uint64_t tensor_id,
+                             uint64_t start, uint64_t bound, unsigned bits, ntt_stream_t stream) {
+  t_launches = 0;
+  if ((word_bytes != 4 && word_bytes != 8) || (!x && count)) return NTT_ERR_ARG;
+  if (bound == 0 && (bits == 0 || bits > 8 * word_bytes)) return NTT_ERR_ARG;
+  if (bound != 0 && word_bytes == 4 && bound > 0xFFFFFFFFull + 1) return NTT_ERR_ARG;
+  cudaError_t e = nttb::launch_synth((int)word_bytes, x, count, seed, tensor_id, start, bound, bits,
+                                     (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_calibrate_butterfly(unsigned log2_beta, uint64_t p, uint64_t W, uint64_t Wp, unsigned iters,
+                                   void* sink, uint64_t* n_butterflies, ntt_stream_t stream) {
+  t_launches = 0;
+  if ((log2_beta != 32 && log2_beta != 64) || !sink || !n_butterflies || !iters) return NTT_ERR_ARG;
+  cudaError_t e = nttb::launch_calib((int)(log2_beta / 8), p, W, Wp, iters, sink, n_butterflies, (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_debug_butterfly(ntt_plan_t pl, int alg, const void* W, const void* Wp, void* X, void* Y, size_t n,
+                               ntt_stream_t stream) {
+  t_launches = 0;
+  if (!pl || (n && (!X || !Y))) return NTT_ERR_ARG;
+  if (alg != 2 && alg != 3 && alg != 4 && alg != 5 && alg != 31 && alg != 41) return NTT_ERR_ARG;
+  if (n && alg != 31 && alg != 41 && (!W || !Wp)) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  cudaError_t e = nttb::launch_debug_bfly((int)pl->wbytes, alg, W, Wp, X, Y, n, pl->p, pl->J, (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+All inputs are seeded.  Sizes span several tiles and ragged batches; the
+config-sized cases run at BASELINE.json's full sizes and compare sampled
+transforms / positions with the oracle (whole transforms where the oracle is
+fast enough) plus size-independent properties.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from gpu_util import P30, P62, RNS, bitrev, rand_residues, root, to_dev, to_host  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ntt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1205_2926_b200 as P
+    return P
+
+
+NTHREADS = oracle.default_threads()
+
+
+def _roundtrip_case(ntt, p, bits, ell, batch, seed, top=False):
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    rng = np.random.default_rng(seed)
+    x = rand_residues(rng, p, (batch, L))
+    if top:  # Alg. 3 accepts [0,2p): exercise the top of the range
+        x = np.where(rng.random((batch, L)) < 0.5, x + np.uint64(p), x)
+        x[:, 0] = 2 * p - 1
+    d = to_dev(x, bits)
+    plan.forward(d)
+    got = to_host(d)
+    ref = oracle.ntt_forward(p, w, x, nthreads=NTHREADS)
+    assert np.array_equal(got, ref), f"forward mismatch p={p} ell={ell} batch={batch}"
+    # inverse accepts [0,4p): feed redundant representatives of the forward output
+    y = got.copy()
+    if top:
+        y = y + np.uint64(p) * rng.integers(0, 4, size=y.shape, dtype=np.uint64)
+    d2 = to_dev(y, bits)
+    plan.inverse(d2)
+    got_inv = to_host(d2)
+    ref_inv = oracle.ntt_inverse(p, w, got, nthreads=NTHREADS)
+    assert np.array_equal(got_inv, ref_inv), f"inverse mismatch p={p} ell={ell}"
+    xr = x.astype(object) % p
+    assert np.array_equal(got_inv.astype(object), (xr * L) % p)  # inverse o forward = L x
+
+
+@pytest.mark.parametrize("ell", list(range(0, 16)))
+def test_single_pass_u32(ntt, ell):
+    _roundtrip_case(ntt, P30, 32, ell, batch=3 if ell > 10 else 37, seed=ell, top=True)
+
+
+@pytest.mark.parametrize("ell", list(range(0, 15)))
+def test_single_pass_u64(ntt, ell):
+    _roundtrip_case(ntt, P62, 64, ell, batch=3 if ell > 10 else 37, seed=100 + ell, top=True)
+
+
+@pytest.mark.parametrize("p,bits,ell,batch", [
+    (P30, 32, 16, 2), (RNS[0], 32, 17, 1), (RNS[1], 32, 20, 1),
+    (P62, 64, 15, 3), (P62, 64, 16, 1), (P62, 64, 18, 1), (P62, 64, 21, 1),
+])
+def test_multi_pass(ntt, p, bits, ell, batch):
+    _roundtrip_case(ntt, p, bits, ell, batch, seed=ell * 7 + bits, top=True)
+
+
+def test_cross_width_identity(ntt):
+    """The same p = 998244353 at beta = 2^32 and 2^64 gives identical outputs."""
+    p, ell = P30, 12
+    w = root(p, 1 << ell)
+    x = rand_residues(np.random.default_rng(9), p, (5, 1 << ell))
+    outs = []
+    for bits in (32, 64):
+        d = to_dev(x, bits)
+        ntt.Plan(p, w, ell, bits).forward(d)
+        outs.append(to_host(d))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_closed_form_delta_and_constant(ntt):
+    """Delta -> all ones; constant c -> (Lc, 0, ...) at a multi-pass length."""
+    for p, bits, ell in ((P62, 64, 20), (P30, 32, 18)):
+        L = 1 << ell
+        plan = ntt.Plan(p, root(p, L), ell, bits)
+        x = np.zeros((2, L), dtype=np.uint64)
+        x[0, 0] = 1
+        x[1, :] = 5
+        d = to_dev(x, bits)
+        plan.forward(d)
+        got = to_host(d)
+        assert (got[0] == 1).all()
+        assert int(got[1, 0]) == 5 * L % p and not got[1, 1:].any()
+
+
+# ------------------------------------------------------------------ BASELINE configs
+def test_config1_single_2p10_u32(ntt):
+    """C1: one forward NTT, L = 2^10, beta = 2^32, p = 998244353, seeded uniform input."""
+    p, ell = P30, 10
+    L = 1 << ell
+    w = root(p, L)
+    assert w == 258648936
+    x = synth.uniform_mod(synth.config_seed(1), 0, 0, L, p)
+    d = to_dev(x, 32)
+    ntt.Plan(p, w, ell, 32).forward(d)
+    got = to_host(d)
+    assert np.array_equal(got, oracle.ntt_forward(p, w, x))
+    b = oracle.dft_direct(p, w, x)  # the definition
+    assert all(int(got[j]) == int(b[bitrev(j, ell)]) for j in range(L))
+
+
+def test_config2_batched_2p12_u64_fwd_inv(ntt):
+    """C2: 4096 transforms of L = 2^12, beta = 2^64; inverse o forward = L x (all 4096)."""
+    p, ell, batch = P62, 12, 4096
+    L = 1 << ell
+    w = root(p, L)
+    assert w == 3233568307201063014
+    plan = ntt.Plan(p, w, ell, 64)
+    d = torch.empty(batch * L, dtype=torch.uint64, device="cuda")
+    ntt.synth_uniform(d, synth.config_seed(2), 0, bound=p)
+    x = to_host(d).reshape(batch, L)
+    plan.forward(d)
+    fwd = to_host(d).reshape(batch, L)
+    sample = np.r_[0:8, 2040:2048, batch - 8:batch]
+    assert np.array_equal(fwd[sample], oracle.ntt_forward(p, w, x[sample], nthreads=NTHREADS))
+    plan.inverse(d)
+    inv = to_host(d).reshape(batch, L)
+    assert np.array_equal(inv, ((x.astype(object) * L) % p).astype(np.uint64))
+
+
+def test_config3_rns_convolution(ntt):
+    """C3: 1024 pairs of 2^15-coefficient polynomials (coeffs < 2^20) zero-padded to 2^16,
+    cyclic convolution mod each of the three primes; sampled pairs vs the oracle."""
+    ell, npairs, half = 16, 1024, 1 << 15
+    L = 1 << ell
+    a = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
+    b = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
+    ntt.synth_uniform(a[:, :half].contiguous().view(-1), synth.config_seed(3), 0, bits=20)  # layout check below
+    ah = synth.uniform_bits(synth.config_seed(3), 0, 0, npairs * half, 20).reshape(npairs, half)
+    bh = synth.uniform_bits(synth.config_seed(3), 1, 0, npairs * half, 20).reshape(npairs, half)
+    a[:, :half] = torch.from_numpy(ah.astype(np.uint32)).cuda()
+    b[:, :half] = torch.from_numpy(bh.astype(np.uint32)).cuda()
+    for p in RNS:
+        plan = ntt.Plan(p, root(p, L), ell, 32)
+        ca, cb = a.clone(), b.clone()
+        plan.cyclic_convolve(ca, cb)
+        got = to_host(ca)
+        for i in (0, 511, npairs - 1):
+            pa = np.zeros(L, dtype=np.uint64); pa[:half] = ah[i]
+            pb = np.zeros(L, dtype=np.uint64); pb[:half] = bh[i]
+            w = root(p, L)
+            ref = oracle.ntt_inverse(p, w, oracle.pointwise(p, oracle.ntt_forward(p, w, pa), oracle.ntt_forward(p, w, pb),
+                                                            scale_L=L))
+            assert np.array_equal(got[i], ref)
+            for k in (0, 1, half, L - 2, L - 1):  # the definition, coefficient by coefficient
+                assert int(got[i, k]) == oracle.cyclic_conv_coeff(p, pa, pb, k)
+
+
+def test_config4_batched_2p24_u64(ntt):
+    """C4: 64 transforms of L = 2^24 (8 GiB); transforms 0 and 63 fully vs the oracle,
+    sampled positions of others by Horner evaluation."""
+    p, ell, batch = P62, 24, 64
+    L = 1 << ell
+    w = root(p, L)
+    assert w == 3854271288527505563
+    plan = ntt.Plan(p, w, ell, 64)
+    d = torch.empty(batch * L, dtype=torch.uint64, device="cuda")
+    ntt.synth_uniform(d, synth.config_seed(4), 0, bound=p)
+    x0 = to_host(d[:L])
+    x63 = to_host(d[63 * L:])
+    x17 = to_host(d[17 * L:18 * L])
+    plan.forward(d)
+    assert np.array_equal(to_host(d[:L]), oracle.ntt_forward(p, w, x0, nthreads=NTHREADS))
+    assert np.array_equal(to_host(d[63 * L:]), oracle.ntt_forward(p, w, x63, nthreads=NTHREADS))
+    got17 = to_host(d[17 * L:18 * L])
+    for j in (0, 1, 12345, L // 2 + 3, L - 1):
+        assert int(got17[j]) == oracle.ntt_output_at(p, w, x17, j)
+
+
+def test_config5_single_2p28_u64(ntt):
+    """C5: one forward NTT of L = 2^28 (2 GiB) on one GPU; whole output vs the oracle."""
+    p, ell = P62, 28
+    L = 1 << ell
+    w = root(p, L)
+    assert w == 796245258878702573
+    plan = ntt.Plan(p, w, ell, 64)
+    d = torch.empty(L, dtype=torch.uint64, device="cuda")
+    ntt.synth_uniform(d, synth.config_seed(5), 0, bound=p)
+    x = to_host(d)
+    plan.forward(d)
+    got = to_host(d)
+    del d
+    torch.cuda.empty_cache()
+    for j in (0, 1, 7, L // 3, L - 1):
+        assert int(got[j]) == oracle.ntt_output_at(p, w, x, j)
+    ref = oracle.ntt_forward(p, w, x, nthreads=NTHREADS)
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ pieces
+def test_pointwise(ntt):
+    for p, bits in ((P30, 32), (P62, 64)):
+        ell = 8
+        L = 1 << ell
+        plan = ntt.Plan(p, root(p, L), ell, bits)
+        rng = np.random.default_rng(3)
+        a = rand_residues(rng, 2 * p, (4, L))  # [0,2p) accepted
+        b = rand_residues(rng, 2 * p, (4, L))
+        a[0, 0] = b[0, 0] = 2 * p - 1
+        for scale in (False, True):
+            da, db = to_dev(a, bits), to_dev(b, bits)
+            dc = torch.empty_like(da)
+            plan.pointwise_mul(dc, da, db, scale_inv_L=scale)
+            ref = oracle.pointwise(p, a, b, scale_L=L if scale else 0)
+            assert np.array_equal(to_host(dc), ref)
+
+
+def test_twiddle_table(ntt):
+    """A1: W_e = omega^e and W'_e = floor(W_e beta/p), i.e. W' p <= W beta < (W'+1) p."""
+    for p, bits, ell in ((P30, 32, 10), (P62, 64, 12), (P62, 64, 20)):
+        L = 1 << ell
+        w = root(p, L)
+        W, Wp = ntt.Plan(p, w, ell, bits).twiddles()
+        beta = 1 << bits
+        for e in list(range(0, 64)) + list(range(L // 2 - 64, L // 2)):
+            We, Wpe = int(W[e]), int(Wp[e])
+            assert We == pow(w, e, p)
+            assert Wpe * p <= We * beta < (Wpe + 1) * p
+
+
+@pytest.mark.parametrize("bits,p", [(32, P30), (64, P62), (32, 167772161)])
+def test_butterflies_bitexact_vs_paper_model(ntt, bits, p):
+    """Each device butterfly reproduces the oracle's step-by-step model of Algorithms
+    2-5 exactly (including the redundant representative)."""
+    rng = np.random.default_rng(bits)
+    n = 1 << 16
+    plan = ntt.Plan(p, root(p, 4), 2, bits)
+    beta = 1 << bits
+    J = pow(p, -1, beta)
+    W = rng.integers(1, p, size=n, dtype=np.uint64)
+    for alg, in_b in ((2, 1), (3, 2), (4, 4), (5, 2), (31, 2), (41, 4)):
+        X = rand_residues(rng, in_b * p, n)
+        Y = rand_residues(rng, in_b * p, n)
+        X[:4] = [0, in_b * p - 1, 0, in_b * p - 1]
+        Y[:4] = [0, 0, in_b * p - 1, in_b * p - 1]
+        Wa = np.ones(n, dtype=np.uint64) if alg in (31, 41) else W
+        if alg == 5:
+            Wp = np.array([(int(w_) * beta) % p for w_ in Wa], dtype=np.uint64)
+        else:
+            Wp = np.array([(int(w_) * beta) // p for w_ in Wa], dtype=np.uint64)
+        dX, dY = to_dev(X, bits), to_dev(Y, bits)
+        plan.debug_butterfly(alg, to_dev(Wa, bits), to_dev(Wp, bits), dX, dY)
+        gx, gy = to_host(dX), to_host(dY)
+        if alg in (31, 41):
+            # W = 1 fast paths: congruence + range (their representative differs from Shoup's)
+            if alg == 31:
+                assert np.array_equal(gx.astype(object) % p, (X.astype(object) + Y) % p)
+                assert np.array_equal(gy.astype(object) % p, (X.astype(object) - Y.astype(object)) % p)
+                assert (gx < 2 * p).all() and (gy < 2 * p).all()
+            else:
+                assert np.array_equal(gx.astype(object) % p, (X.astype(object) + Y) % p)
+                assert np.array_equal(gy.astype(object) % p, (X.astype(object) - Y.astype(object)) % p)
+                assert (gx < 4 * p).all() and (gy < 4 * p).all()
+            continue
+        ox, oy = oracle.bfly(alg, bits, p, Wa, Wp, X, Y, J=J)
+        assert np.array_equal(gx, ox) and np.array_equal(gy, oy), alg
+
+
+def test_synth_matches_host_generator(ntt):
+    for bits, bound, kbits in ((64, P62, 0), (32, P30, 0), (32, 0, 20), (64, 0, 61)):
+        d = torch.empty(100_003, dtype=torch.uint64 if bits == 64 else torch.uint32, device="cuda")
+        ntt.synth_uniform(d, 77, 5, start=1000, bound=bound, bits=kbits)
+        host = (synth.uniform_mod(77, 5, 1000, d.numel(), bound) if bound
+                else synth.uniform_bits(77, 5, 1000, d.numel(), kbits))
+        assert np.array_equal(to_host(d), host)
+
+
+def test_edge_cases(ntt):
+    import ctypes
+    p, ell = P62, 10
+    plan = ntt.Plan(p, root(p, 1 << ell), ell, 64)
+    d = torch.zeros(1 << ell, dtype=torch.uint64, device="cuda")
+    plan.forward(d, batch=0)  # no-op
+    lib = ntt.lib()
+    # misaligned pointer -> NTT_ERR_ARG
+    assert lib.ntt_forward(plan.handle, d.data_ptr() + 8, 1, 0) == -1
+    assert lib.ntt_forward(plan.handle, None, 1, 0) == -1
+    # ell = 0: identity (only normalisation)
+    p0 = ntt.Plan(P30, 1, 0, 32)
+    t = to_dev(np.array([5, P30 + 3, 2 * P30 - 1], dtype=np.uint64), 32)
+    p0.forward(t)
+    assert list(to_host(t)) == [5, 3, P30 - 1]
+    # all-(2p-1) input at the edge of Alg. 3's range
+    x = np.full((2, 1 << ell), 2 * p - 1, dtype=np.uint64)
+    dx = to_dev(x, 64)
+    plan.forward(dx)
+    assert np.array_equal(to_host(dx), oracle.ntt_forward(p, root(p, 1 << ell), x))
