@@ -209,7 +209,8 @@ def run_native(args, cfg, rank, world, local_rank):
     step_ms, kernel_ms, launches = [], {}, 0
     for _ in range(args.steps):
         reset_inputs()
-        flush.zero_()  # L2 flush between timed steps (outside the events)
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps, on the timed stream, before the start event
         start = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         evs = []

@@ -14,6 +14,10 @@ constexpr int kContigMaxLog32 = 15;  // 2^15 u32 = 128 KiB smem, 1024 threads x 
 constexpr int kColsMaxLog64 = 9;     // 2^9 rows x 16 u64 columns = 64 KiB tile
 constexpr int kColsMaxLog32 = 10;    // 2^10 rows x 32 u32 columns = 128 KiB tile
 constexpr int kColsMinLog = 4;
+// TMA-staged single-pass kernel (ntt_contig_tma.cu): double-buffered tiles of <= 64 KiB
+constexpr int kTmaMinLog = 8;
+constexpr int kTmaMaxLog64 = 13;
+constexpr int kTmaMaxLog32 = 14;
 
 // Column-pass geometry (four-step pass j of the nested decomposition):
 // the data is viewed as blocks of B = N*S words; inside a block, element
@@ -46,6 +50,9 @@ struct DevTables {
 // launchers (return cudaGetLastError of the launch)
 cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch, const void* tw,
                           uint64_t p, cudaStream_t s);
+bool tma_supported(int wbytes, int logn);
+cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
+                              const void* tw, uint64_t p, cudaStream_t s);
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
                         uint64_t p, cudaStream_t s);
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,

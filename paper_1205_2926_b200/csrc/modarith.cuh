@@ -17,20 +17,57 @@ __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umu
 
 template <class W> __device__ __forceinline__ W csub(W x, W m) { return x >= m ? x - m : x; }
 
+// Modulus context kept in registers: p, 2p and (for beta = 2^64 with
+// p = 1 mod 2^32) np1 = -(p >> 32) mod 2^32, which turns lo64(Q p) into one IMAD.
+template <class W> struct Mod {
+  W p, p2;
+  uint32_t np1;
+};
+template <class W> __device__ __forceinline__ Mod<W> make_mod(W p) {
+  Mod<W> m;
+  m.p = p;
+  m.p2 = 2 * p;
+  m.np1 = (uint32_t)(0u - (uint32_t)((uint64_t)p >> 32));
+  return m;
+}
+
 // Shoup multiplication (Theorem 1 bound P:85): for any T < beta,
 // returns WT - Qp in [0, 2p), congruent to W*T mod p, Q = floor(W'T/beta).
+// PLO1 (beta = 2^64, p = 1 mod 2^32): Qp mod beta = Q + (q0 * p_hi) << 32, so the
+// low product costs one 32-bit IMAD instead of a 64 x 64 -> 64 multiply.
+template <class W, bool PLO1 = false> __device__ __forceinline__ W shoup_mul(W T, W w, W wp, const Mod<W>& m) {
+  W Q = mulhi(wp, T);
+  if constexpr (sizeof(W) == 8 && PLO1) {
+    const uint64_t WT = (uint64_t)w * (uint64_t)T;
+    uint64_t r;
+    asm("{\n\t.reg .u32 q0,q1,r0,r1;\n\t"
+        "mov.b64 {q0,q1}, %1;\n\tmov.b64 {r0,r1}, %2;\n\t"
+        "sub.cc.u32 r0, r0, q0;\n\tsubc.u32 r1, r1, q1;\n\t"
+        "mad.lo.u32 r1, q0, %3, r1;\n\t"
+        "mov.b64 %0, {r0,r1};\n\t}"
+        : "=l"(r) : "l"((uint64_t)Q), "l"(WT), "r"(m.np1));
+    return (W)r;
+  } else {
+    return w * T - Q * m.p;  // mod beta
+  }
+}
+// Plain-modulus overload (pointwise / debug paths).
 template <class W> __device__ __forceinline__ W shoup_mul(W T, W w, W wp, W p) {
   W Q = mulhi(wp, T);
-  return w * T - Q * p;  // mod beta
+  return w * T - Q * p;
 }
 
 // Algorithm 3, the modified Shoup butterfly:
 // X, Y in [0,2p) -> X' = X+Y, Y' = W(X-Y), both in [0,2p)  (Theorem 2).
-template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, W p, W p2) {
-  W s = csub<W>(X + Y, p2);   // lines 1-2
-  W T = X - Y + p2;           // line 3: T in [0,4p), no correction
-  Y = shoup_mul<W>(T, w, wp, p);  // lines 4-5: [0,2p), no correction
+template <class W, bool PLO1 = false>
+__device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  W s = csub<W>(X + Y, m.p2);  // lines 1-2
+  W T = X - Y + m.p2;          // line 3: T in [0,4p), no correction
+  Y = shoup_mul<W, PLO1>(T, w, wp, m);  // lines 4-5: [0,2p), no correction
   X = s;
+}
+template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, W p, W p2) {
+  bfly_alg3<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u});
 }
 
 // W = 1 butterflies (O(L) butterflies have W = 1 and are cheaper):
@@ -44,11 +81,15 @@ template <class W> __device__ __forceinline__ void bfly_alg3_w1(W& X, W& Y, W p2
 
 // Algorithm 4, the modified inverse butterfly:
 // X, Y in [0,4p) -> X' = X + WY, Y' = X - WY, both in [0,4p)  (Theorem 3).
-template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, W p, W p2) {
-  W x = csub<W>(X, p2);            // line 1
-  W T = shoup_mul<W>(Y, w, wp, p);  // lines 2-3: Y < 4p < beta is a legal Shoup input
+template <class W, bool PLO1 = false>
+__device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  W x = csub<W>(X, m.p2);                   // line 1
+  W T = shoup_mul<W, PLO1>(Y, w, wp, m);    // lines 2-3: Y < 4p < beta is a legal Shoup input
   X = x + T;
-  Y = x - T + p2;
+  Y = x - T + m.p2;
+}
+template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, W p, W p2) {
+  bfly_alg4<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u});
 }
 
 // W = 1 inverse butterfly: T = Y reduced once by 2p (Y < 4p -> T < 2p).

@@ -1,0 +1,322 @@
+// ntt_contig_tma.cu -- the on-chip (single-pass) transform with TMA staging.
+//
+// Each persistent CTA walks tiles of K consecutive transforms.  A tile is
+// brought into shared memory by the Tensor Memory Accelerator
+// (cp.async.bulk.tensor.2d, SWIZZLE_128B) while the CTA computes the previous
+// tile (two buffers, one mbarrier each), so HBM latency is off the critical
+// path and no registers are spent on loads.  The rounds of rounds.cuh then run
+// out of the swizzled buffer: the TMA 128-byte swizzle (16-byte chunk index
+// XOR row mod 8) keeps every round's access pattern bank-conflict free when
+// contiguous runs are read as 16-byte vectors (tools/bank_sim.py).  The last
+// round writes its results back into the tile, which leaves through one TMA bulk
+// tensor store (cp.async.bulk.tensor.2d.global.shared::cta), so both the
+// bit-reversed forward output and the natural-order inverse output are written
+// as full 128-byte rows.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "modarith.cuh"
+#include "rounds.cuh"
+
+namespace nttb {
+
+// ----------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Element index -> swizzled element index under SWIZZLE_128B (16-byte chunk ^= 128-byte row mod 8).
+template <class W> __device__ __forceinline__ int tswz(int i) {
+  if constexpr (sizeof(W) == 8) return i ^ (((i >> 4) & 7) << 1);
+  else return i ^ (((i >> 5) & 7) << 2);
+}
+
+// ----------------------------------------------------------------- shape
+template <class W, int LOGN, int LE> struct TmaShape {
+  static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E;
+  static constexpr int K = T >= 256 ? 1 : 256 / T;   // transforms per tile
+  static constexpr int THREADS = K * T;
+  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
+  static constexpr int TILE_WORDS = K * N;
+  static constexpr int TILE_BYTES = TILE_WORDS * (int)sizeof(W);
+  static constexpr int ROW_WORDS = 128 / (int)sizeof(W);
+  static constexpr int TILE_ROWS = TILE_WORDS / ROW_WORDS;
+  static constexpr int BOX_ROWS = TILE_ROWS < 256 ? TILE_ROWS : 256;
+  static constexpr int BOXES = TILE_ROWS / BOX_ROWS;
+  static constexpr int BOX_BYTES = BOX_ROWS * 128;
+  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + 1024;
+  using RC = Rounds<LOGN, LE>;
+  static constexpr int R = RC::R;
+  static_assert(R >= 2, "TMA kernel needs at least one exchange");
+  static_assert(N * sizeof(W) % 1024 == 0, "slot buffers must keep the 1024-byte swizzle period");
+};
+
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
+__device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t, bool active,
+                                          const TwPair<W>* __restrict__ tw, const Mod<W>& m, bool norm,
+                                          bool first_exchange, const CUtensorMap* map, size_t next_tile,
+                                          size_t ntiles, uint32_t next_buf, uint32_t next_bar) {
+  using Sh = TmaShape<W, LOGN, LE>;
+  using RC = typename Sh::RC;
+  constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
+  constexpr int S = 1 << SR, G = Sh::E >> SR;
+  constexpr int D = Sh::N >> (LEVEL + SR), B = Sh::N >> LEVEL;
+  constexpr int PER = 16 / (int)sizeof(W);
+  constexpr bool VEC = (D == 1) && (S >= PER);
+  int c[G], blk[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = t + Sh::T * q;
+    blk[q] = g / D;
+    c[q] = g % D;
+  }
+  constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
+  // ---- load from the swizzled tile buffer
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    if constexpr (VEC) {
+#pragma unroll
+      for (int h = 0; h < S; h += PER)
+        unpack16<W>(*reinterpret_cast<const uint4*>(sb + tswz<W>(blk[q] * B + h)), v + q * S + h);
+    } else {
+#pragma unroll
+      for (int h = 0; h < S; ++h) v[q * S + h] = sb[tswz<W>(blk[q] * B + h * D + c[q])];
+    }
+  }
+  // ---- compute
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  if constexpr (last) {
+    if (norm) {
+#pragma unroll
+      for (int i = 0; i < Sh::E; ++i) v[i] = INV ? norm4<W>(v[i], m.p, m.p2) : norm2<W>(v[i], m.p);
+    }
+    // each thread writes back exactly the positions it read (no cross-thread hazard),
+    // then the tile leaves through one TMA bulk tensor store (see k_contig_tma)
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if constexpr (VEC) {
+#pragma unroll
+        for (int h = 0; h < S; h += PER)
+          *reinterpret_cast<uint4*>(sb + tswz<W>(blk[q] * B + h)) = pack16<W>(v + q * S + h);
+      } else {
+#pragma unroll
+        for (int h = 0; h < S; ++h) sb[tswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
+      }
+    }
+    (void)xb;
+    (void)active;
+  } else {
+    __syncthreads();
+    if (first_exchange && threadIdx.x == 0 && next_tile < ntiles) {
+      // every thread has finished the previous tile (the other buffer): once its TMA
+      // store has read the buffer, prefetch the next tile into it
+      bulk_wait_read0();
+      mbar_expect_tx(next_bar, Sh::TILE_BYTES);
+      const int row0 = (int)(next_tile * Sh::TILE_ROWS);
+#pragma unroll
+      for (int bx = 0; bx < Sh::BOXES; ++bx)
+        tma_load_2d(next_buf + bx * Sh::BOX_BYTES, map, 0, row0 + bx * Sh::BOX_ROWS, next_bar);
+    }
+    // ---- exchange (same positions as this round's load)
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if constexpr (VEC) {
+#pragma unroll
+        for (int h = 0; h < S; h += PER)
+          *reinterpret_cast<uint4*>(sb + tswz<W>(blk[q] * B + h)) = pack16<W>(v + q * S + h);
+      } else {
+#pragma unroll
+        for (int h = 0; h < S; ++h) sb[tswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
+      }
+    }
+    __syncthreads();
+    constexpr int nr = INV ? r - 1 : r + 1;
+    tma_round<W, LOGN, LE, INV, PLO1, nr>(v, xb, sb, t, active, tw, m, norm, false, map, next_tile, ntiles, next_buf,
+                                          next_bar);
+  }
+}
+
+template <class W, int LOGN, int LE, bool INV, bool PLO1>
+__global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LOGN, LE>::MINB)
+    k_contig_tma(const __grid_constant__ CUtensorMap tmap, W* __restrict__ x, size_t batch,
+                 const TwPair<W>* __restrict__ tw, W p, int norm) {
+  using Sh = TmaShape<W, LOGN, LE>;
+  extern __shared__ unsigned char smem_raw[];
+  uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023;
+  W* buf[2] = {reinterpret_cast<W*>(base), reinterpret_cast<W*>(base + Sh::TILE_BYTES)};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * (size_t)Sh::TILE_BYTES);
+  const uint32_t bar_a[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
+  const int slot = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+  const Mod<W> m = make_mod<W>(p);
+  const size_t ntiles = (batch + Sh::K - 1) / Sh::K;
+  if (threadIdx.x == 0) {
+    mbar_init(bar_a[0], 1);
+    mbar_init(bar_a[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  size_t tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < ntiles) {
+    mbar_expect_tx(bar_a[0], Sh::TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < Sh::BOXES; ++bx)
+      tma_load_2d(smem_u32(buf[0]) + bx * Sh::BOX_BYTES, &tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
+                  bar_a[0]);
+  }
+  W v[Sh::E];
+  for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int cur = it & 1;
+    mbar_wait(bar_a[cur], (it >> 1) & 1);
+    const size_t b = tile * Sh::K + slot;
+    const bool active = b < batch;
+    constexpr int r0 = INV ? Sh::R - 1 : 0;
+    tma_round<W, LOGN, LE, INV, PLO1, r0>(v, x + b * Sh::N, buf[cur] + slot * Sh::N, t, active, tw, m, norm != 0, true,
+                                          &tmap, tile + gridDim.x, ntiles, smem_u32(buf[cur ^ 1]), bar_a[cur ^ 1]);
+    fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {  // rows past the tensor end (partial last tile) are clipped by TMA
+#pragma unroll
+      for (int bx = 0; bx < Sh::BOXES; ++bx)
+        tma_store_2d(&tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
+                     smem_u32(buf[cur]) + bx * Sh::BOX_BYTES);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();  // smem must outlive the last bulk store
+}
+
+// ----------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <class W> struct TmaLE {
+  static constexpr int value = 4 + (sizeof(W) == 4 ? 1 : 0);
+};
+
+template <class W, int LOGN, bool INV, bool PLO1>
+static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bool norm, cudaStream_t s) {
+  constexpr int LE = TmaLE<W>::value;
+  using Sh = TmaShape<W, LOGN, LE>;
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const uint64_t rows = (uint64_t)batch * Sh::N / Sh::ROW_WORDS;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)Sh::ROW_WORDS, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {(cuuint32_t)Sh::ROW_WORDS, (cuuint32_t)Sh::BOX_ROWS};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, x, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  auto kern = k_contig_tma<W, LOGN, LE, INV, PLO1>;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Sh::THREADS, Sh::SMEM);
+    if (occ <= 0) occ = 1;
+  }
+  const size_t ntiles = (batch + Sh::K - 1) / Sh::K;
+  const size_t maxg = (size_t)occ * sm_count();
+  const unsigned grid = (unsigned)(ntiles < maxg ? ntiles : maxg);
+  if (!grid) return cudaSuccess;
+  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(map, reinterpret_cast<W*>(x), batch,
+                                           reinterpret_cast<const TwPair<W>*>(tw), (W)p, norm ? 1 : 0);
+  return cudaGetLastError();
+}
+
+template <class W, bool INV, int LO, int HI>
+static cudaError_t tma_dispatch(int logn, void* x, size_t batch, const void* tw, uint64_t p, bool norm,
+                                cudaStream_t s) {
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (logn == LO) {
+      if constexpr (sizeof(W) == 8) {
+        if ((p & 0xffffffffull) == 1) return run_tma<W, LO, INV, true>(x, batch, tw, p, norm, s);
+      }
+      return run_tma<W, LO, INV, false>(x, batch, tw, p, norm, s);
+    }
+    return tma_dispatch<W, INV, LO + 1, HI>(logn, x, batch, tw, p, norm, s);
+  }
+}
+
+bool tma_supported(int wbytes, int logn) {
+  return wbytes == 8 ? (logn >= kTmaMinLog && logn <= kTmaMaxLog64) : (logn >= kTmaMinLog && logn <= kTmaMaxLog32);
+}
+
+cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
+                              const void* tw, uint64_t p, cudaStream_t s) {
+  if (wbytes == 8)
+    return inverse ? tma_dispatch<uint64_t, true, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s)
+                   : tma_dispatch<uint64_t, false, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
+  return inverse ? tma_dispatch<uint32_t, true, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s)
+                 : tma_dispatch<uint32_t, false, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
+}
+
+}  // namespace nttb

@@ -13,135 +13,16 @@
 
 #include "internal.h"
 #include "modarith.cuh"
+#include "rounds.cuh"
 
 namespace nttb {
 
 // ----------------------------------------------------------------- helpers
-template <class W> __device__ __forceinline__ void ldtw(const TwPair<W>* tw, uint32_t e, W& w, W& wp);
-template <> __device__ __forceinline__ void ldtw<uint64_t>(const TwPair<uint64_t>* tw, uint32_t e, uint64_t& w,
-                                                           uint64_t& wp) {
-  ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(tw) + e);
-  w = t.x;
-  wp = t.y;
-}
-template <> __device__ __forceinline__ void ldtw<uint32_t>(const TwPair<uint32_t>* tw, uint32_t e, uint32_t& w,
-                                                           uint32_t& wp) {
-  uint2 t = __ldg(reinterpret_cast<const uint2*>(tw) + e);
-  w = t.x;
-  wp = t.y;
-}
-
-// XOR swizzle of the word index inside a 128-byte smem row, so that the
-// strided exchange patterns of every round hit distinct banks.
+// XOR swizzle of the word index inside a 128-byte smem row (v1 kernel), so that
+// the strided exchange patterns of every round hit distinct banks.
 template <class W> __device__ __forceinline__ int swz(int i) {
   constexpr int S = sizeof(W) == 8 ? 4 : 5;
   return i ^ ((i >> S) & ((1 << S) - 1));
-}
-
-// Contiguous run of S words: widest aligned vector accesses.
-template <class W, int S> __device__ __forceinline__ void load_run(const W* src, W* v) {
-  if constexpr (S * sizeof(W) >= 16) {
-    constexpr int PER = 16 / sizeof(W);
-#pragma unroll
-    for (int i = 0; i < S / PER; ++i) {
-      uint4 u = *reinterpret_cast<const uint4*>(src + i * PER);
-      if constexpr (sizeof(W) == 8) {
-        v[2 * i] = ((uint64_t)u.y << 32) | u.x;
-        v[2 * i + 1] = ((uint64_t)u.w << 32) | u.z;
-      } else {
-        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < S; ++i) v[i] = src[i];
-  }
-}
-template <class W, int S> __device__ __forceinline__ void store_run(W* dst, const W* v) {
-  if constexpr (S * sizeof(W) >= 16) {
-    constexpr int PER = 16 / sizeof(W);
-#pragma unroll
-    for (int i = 0; i < S / PER; ++i) {
-      uint4 u;
-      if constexpr (sizeof(W) == 8) {
-        u.x = (uint32_t)v[2 * i]; u.y = (uint32_t)(v[2 * i] >> 32);
-        u.z = (uint32_t)v[2 * i + 1]; u.w = (uint32_t)(v[2 * i + 1] >> 32);
-      } else {
-        u.x = v[4 * i]; u.y = v[4 * i + 1]; u.z = v[4 * i + 2]; u.w = v[4 * i + 3];
-      }
-      *reinterpret_cast<uint4*>(dst + i * PER) = u;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < S; ++i) dst[i] = v[i];
-  }
-}
-
-// Round structure: R rounds of balanced stage counts sr(r) <= LE.
-template <int LOGN, int LE> struct Rounds {
-  static constexpr int R = (LOGN + LE - 1) / LE;
-  __host__ __device__ static constexpr int sr(int r) { return LOGN / R + (r < LOGN % R ? 1 : 0); }
-  __host__ __device__ static constexpr int level(int r) {
-    int s = 0;
-    for (int i = 0; i < r; ++i) s += sr(i);
-    return s;
-  }
-};
-
-// One forward round: stages LEVEL+1 .. LEVEL+SR of Algorithm 1 on G groups of
-// 2^SR words.  Group q holds positions blk*B + h*D + c[q] (h < 2^SR) of an
-// N-point transform; stage i = LEVEL+1+j uses twiddle zeta_i^k = omega^{2^{i-1} k}
-// with k = (h mod half)*D + c, read from the table omega^e, e < N/2.
-template <class W, int LOGN, int SR, int LEVEL, int G>
-__device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, W p, W p2) {
-  constexpr int S = 1 << SR;
-  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
-#pragma unroll
-  for (int j = 0; j < SR; ++j) {
-    const int half = S >> (j + 1);
-    const bool w1 = (LEVEL + j + 1 == LOGN);  // last stage: m = 1, every twiddle is 1
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-#pragma unroll
-      for (int hh = 0; hh < half; ++hh) {
-        W w = 1, wp = 0;
-        if (!w1) ldtw<W>(tw, (uint32_t)(hh * D + c[q]) << (LEVEL + j), w, wp);
-#pragma unroll
-        for (int b = 0; b < (1 << j); ++b) {
-          const int h = b * 2 * half + hh;
-          if (w1) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], p2);
-          else bfly_alg3<W>(v[q * S + h], v[q * S + h + half], w, wp, p, p2);
-        }
-      }
-    }
-  }
-}
-
-// One inverse round: the same stages run backwards, Algorithm 4 with
-// twiddle omega^{-2^{i-1} k} from the inverse table.
-template <class W, int LOGN, int SR, int LEVEL, int G>
-__device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, W p, W p2) {
-  constexpr int S = 1 << SR;
-  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
-#pragma unroll
-  for (int j = SR - 1; j >= 0; --j) {
-    const int half = S >> (j + 1);
-    const bool w1 = (LEVEL + j + 1 == LOGN);
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-#pragma unroll
-      for (int hh = 0; hh < half; ++hh) {
-        W w = 1, wp = 0;
-        if (!w1) ldtw<W>(twi, (uint32_t)(hh * D + c[q]) << (LEVEL + j), w, wp);
-#pragma unroll
-        for (int b = 0; b < (1 << j); ++b) {
-          const int h = b * 2 * half + hh;
-          if (w1) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], p2);
-          else bfly_alg4<W>(v[q * S + h], v[q * S + h + half], w, wp, p, p2);
-        }
-      }
-    }
-  }
 }
 
 // ----------------------------------------------------------------- contiguous single-pass kernel
@@ -165,10 +46,11 @@ struct GatherArgs {
   uint32_t log_rows_local;    // log2(N1/G): rows per block
 };
 
-template <class W, int LOGN, int LE, bool INV, bool GATHER, int r>
+template <class W, int LOGN, int LE, bool INV, bool GATHER, bool PLO1, int r>
 __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* __restrict__ gin, size_t row,
                                              const GatherArgs& ga, W* sb, int t, bool active,
-                                             const TwPair<W>* __restrict__ tw, W p, W p2, bool norm) {
+                                             const TwPair<W>* __restrict__ tw, const Mod<W>& m, bool norm) {
+  const W p = m.p, p2 = m.p2;
   using Sh = ContigShape<LOGN, LE>;
   using RC = typename Sh::RC;
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
@@ -218,8 +100,8 @@ __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* 
       for (int h = 0; h < S; ++h) v[q * S + h] = sb[swz<W>(blk[q] * B + h * D + c[q])];
   }
   // ---- compute
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
-  else dit_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   // ---- store
   if constexpr (last) {
     if (norm) {
@@ -245,26 +127,26 @@ __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* 
       for (int h = 0; h < S; ++h) sb[swz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    contig_round<W, LOGN, LE, INV, GATHER, nr>(v, xb, gin, row, ga, sb, t, active, tw, p, p2, norm);
+    contig_round<W, LOGN, LE, INV, GATHER, PLO1, nr>(v, xb, gin, row, ga, sb, t, active, tw, m, norm);
   }
 }
 
-template <class W, int LOGN, int LE, bool INV, bool GATHER>
+template <class W, int LOGN, int LE, bool INV, bool GATHER, bool PLO1>
 __global__ void __launch_bounds__(ContigShape<LOGN, LE>::THREADS, ContigShape<LOGN, LE>::MINB)
     k_contig(W* __restrict__ x, size_t batch, const TwPair<W>* __restrict__ tw, W p, int norm, GatherArgs ga) {
   using Sh = ContigShape<LOGN, LE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* sm = reinterpret_cast<W*>(smem_raw);
   const int slot = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
-  const W p2 = 2 * p;
+  const Mod<W> m = make_mod<W>(p);
   W v[Sh::E];
   for (size_t b0 = (size_t)blockIdx.x * Sh::K; b0 < batch; b0 += (size_t)gridDim.x * Sh::K) {
     const size_t b = b0 + slot;
     const bool active = b < batch;
     W* xb = x + b * Sh::N;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    contig_round<W, LOGN, LE, INV, GATHER, r0>(v, xb, reinterpret_cast<const W*>(ga.in), b, ga, sm + slot * Sh::N, t,
-                                               active, tw, p, p2, norm != 0);
+    contig_round<W, LOGN, LE, INV, GATHER, PLO1, r0>(v, xb, reinterpret_cast<const W*>(ga.in), b, ga, sm + slot * Sh::N,
+                                                     t, active, tw, m, norm != 0);
   }
 }
 
@@ -281,25 +163,26 @@ template <class W, int LOGN, int LE> struct ColsShape {
   static constexpr int R = RC::R;
 };
 
-template <class W>
+template <class W, bool PLO1>
 __device__ __forceinline__ W fourstep_twiddle(W val, uint32_t e, const ColsParams& prm, const TwPair<W>* __restrict__ fa,
-                                              const TwPair<W>* __restrict__ fb, W p) {
+                                              const TwPair<W>* __restrict__ fb, const Mod<W>& m) {
   W w, wp;
   if (prm.H == 0) {
     ldtw<W>(fa, e, w, wp);
-    return shoup_mul<W>(val, w, wp, p);
+    return shoup_mul<W, PLO1>(val, w, wp, m);
   }
   ldtw<W>(fb, e & ((1u << prm.H) - 1), w, wp);
-  val = shoup_mul<W>(val, w, wp, p);
+  val = shoup_mul<W, PLO1>(val, w, wp, m);
   ldtw<W>(fa, e >> prm.H, w, wp);
-  return shoup_mul<W>(val, w, wp, p);
+  return shoup_mul<W, PLO1>(val, w, wp, m);
 }
 
-template <class W, int LOGN, int LE, bool INV, int r>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
 __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int t, int cc, uint32_t cglob,
                                            const ColsParams& prm, const TwPair<W>* __restrict__ tw,
-                                           const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p,
-                                           W p2) {
+                                           const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb,
+                                           const Mod<W>& m) {
+  const W p = m.p, p2 = m.p2;
   using Sh = ColsShape<W, LOGN, LE>;
   using RC = typename Sh::RC;
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
@@ -328,7 +211,7 @@ __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int 
             const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
             const uint32_t e = ((cglob * rv) << prm.log_tw_mul);
             const uint32_t einv = (uint32_t)((((uint64_t)1 << prm.ell) - e) & (((uint64_t)1 << prm.ell) - 1));
-            val = fourstep_twiddle<W>(val, einv, prm, fa, fb, p);
+            val = fourstep_twiddle<W, PLO1>(val, einv, prm, fa, fb, m);
           }
         }
         v[q * S + h] = val;
@@ -339,8 +222,8 @@ __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int 
 #pragma unroll
       for (int h = 0; h < S; ++h) v[q * S + h] = sm[(blk[q] * B + h * D + c[q]) * C + cc];
   }
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
-  else dit_round<W, LOGN, SR, LEVEL, G>(v, c, tw, p, p2);
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (last) {
 #pragma unroll
     for (int q = 0; q < G; ++q)
@@ -351,7 +234,7 @@ __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int 
         if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
           if (prm.twiddle) {
             const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
-            val = fourstep_twiddle<W>(val, (cglob * rv) << prm.log_tw_mul, prm, fa, fb, p);
+            val = fourstep_twiddle<W, PLO1>(val, (cglob * rv) << prm.log_tw_mul, prm, fa, fb, m);
           }
           if (prm.normalize) val = norm2<W>(val, p);
         } else {
@@ -367,11 +250,11 @@ __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int 
       for (int h = 0; h < S; ++h) sm[(blk[q] * B + h * D + c[q]) * C + cc] = v[q * S + h];
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    cols_round<W, LOGN, LE, INV, nr>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, p, p2);
+    cols_round<W, LOGN, LE, INV, PLO1, nr>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, m);
   }
 }
 
-template <class W, int LOGN, int LE, bool INV>
+template <class W, int LOGN, int LE, bool INV, bool PLO1>
 __global__ void __launch_bounds__(ColsShape<W, LOGN, LE>::THREADS, ColsShape<W, LOGN, LE>::MINB)
     k_cols(W* __restrict__ x, ColsParams prm, const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
            const TwPair<W>* __restrict__ fb, W p) {
@@ -379,7 +262,7 @@ __global__ void __launch_bounds__(ColsShape<W, LOGN, LE>::THREADS, ColsShape<W, 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* sm = reinterpret_cast<W*>(smem_raw);
   const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
-  const W p2 = 2 * p;
+  const Mod<W> m = make_mod<W>(p);
   W v[Sh::E];
   const uint64_t cg_mask = ((uint64_t)1 << prm.log_colgroups) - 1;
   for (uint64_t tile = blockIdx.x; tile < prm.n_tiles; tile += gridDim.x) {
@@ -393,8 +276,7 @@ __global__ void __launch_bounds__(ColsShape<W, LOGN, LE>::THREADS, ColsShape<W, 
       cglob = (rb << prm.log_n2) | (prm.col0 + cl);
     }
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    cols_round<W, LOGN, LE, INV, r0>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, p, p2);
-    __syncthreads();
+    cols_round<W, LOGN, LE, INV, PLO1, r0>(v, xb, sm, t, cc, cglob, prm, tw, fa, fb, m);
   }
 }
 
@@ -420,18 +302,19 @@ template <class W> __global__ void k_normalize(W* __restrict__ x, size_t n, W p,
     x[i] = from4p ? norm4<W>(x[i], p, p2) : norm2<W>(x[i], p);
 }
 
-template <class W>
+template <class W, bool PLO1>
 __global__ void k_debug_bfly(int alg, const W* __restrict__ Wv, const W* __restrict__ Wpv, W* __restrict__ X,
                              W* __restrict__ Y, size_t n, W p, W J) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   W x = X[i], y = Y[i];
-  const W p2 = 2 * p;
-  switch (alg) {
+  const Mod<W> m = make_mod<W>(p);
+  const W p2 = m.p2;
+  switch (alg) {  // the transform kernels' exact arithmetic (PLO1 when p = 1 mod 2^32)
     case 2: bfly_alg2<W>(x, y, Wv[i], Wpv[i], p); break;
-    case 3: bfly_alg3<W>(x, y, Wv[i], Wpv[i], p, p2); break;
+    case 3: bfly_alg3<W, PLO1>(x, y, Wv[i], Wpv[i], m); break;
     case 31: bfly_alg3_w1<W>(x, y, p2); break;
-    case 4: bfly_alg4<W>(x, y, Wv[i], Wpv[i], p, p2); break;
+    case 4: bfly_alg4<W, PLO1>(x, y, Wv[i], Wpv[i], m); break;
     case 41: bfly_alg4_w1<W>(x, y, p2); break;
     case 5: bfly_alg5<W>(x, y, Wpv[i], J, p, p2); break;
     default: break;
@@ -442,11 +325,11 @@ __global__ void k_debug_bfly(int alg, const W* __restrict__ Wv, const W* __restr
 
 // ----------------------------------------------------------------- ALU calibration
 // Register-only Algorithm 3 loop: 8 independent butterfly chains per thread.
-template <class W>
+template <class W, bool PLO1>
 __global__ void __launch_bounds__(256) k_calib(W* sink, W p, W w, W wp, unsigned iters) {
   constexpr int CH = 8;
   W x[CH], y[CH];
-  const W p2 = 2 * p;
+  const Mod<W> m = make_mod<W>(p);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     x[c] = (W)(threadIdx.x * 7 + c) % p;
@@ -454,7 +337,7 @@ __global__ void __launch_bounds__(256) k_calib(W* sink, W p, W w, W wp, unsigned
   }
   for (unsigned i = 0; i < iters; ++i)
 #pragma unroll
-    for (int c = 0; c < CH; ++c) bfly_alg3<W>(x[c], y[c], w, wp, p, p2);
+    for (int c = 0; c < CH; ++c) bfly_alg3<W, PLO1>(x[c], y[c], w, wp, m);
   W s = 0;
 #pragma unroll
   for (int c = 0; c < CH; ++c) s ^= x[c] ^ y[c];
@@ -486,13 +369,13 @@ template <class W, int LOGN> struct ContigLE {
                                               : (LOGN <= 5 ? LOGN : 5);
 };
 
-template <class W, int LOGN, bool INV, bool GATHER>
+template <class W, int LOGN, bool INV, bool GATHER, bool PLO1>
 static cudaError_t run_contig(void* x, size_t batch, const void* tw, uint64_t p, bool norm, GatherArgs ga,
                               cudaStream_t s) {
   constexpr int LE = ContigLE<W, LOGN>::value;
   using Sh = ContigShape<LOGN, LE>;
   const size_t smem = Sh::R > 1 ? (size_t)Sh::K * Sh::N * sizeof(W) : 0;
-  auto kern = k_contig<W, LOGN, LE, INV, GATHER>;
+  auto kern = k_contig<W, LOGN, LE, INV, GATHER, PLO1>;
   static int occ = 0;
   if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
   const size_t iters = (batch + Sh::K - 1) / Sh::K;
@@ -508,12 +391,12 @@ template <class W, int LOGN> struct ColsLE {
   static constexpr int value = sizeof(W) == 8 ? 4 : (LOGN < 5 ? LOGN : 5);
 };
 
-template <class W, int LOGN, bool INV>
+template <class W, int LOGN, bool INV, bool PLO1>
 static cudaError_t run_cols(void* x, const ColsParams& prm, const DevTables& t, uint64_t p, cudaStream_t s) {
   constexpr int LE = ColsLE<W, LOGN>::value;
   using Sh = ColsShape<W, LOGN, LE>;
   const size_t smem = (size_t)Sh::N * Sh::C * sizeof(W);
-  auto kern = k_cols<W, LOGN, LE, INV>;
+  auto kern = k_cols<W, LOGN, LE, INV, PLO1>;
   static int occ = 0;
   if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
   const uint64_t maxg = (uint64_t)occ * num_sms();
@@ -533,7 +416,12 @@ static cudaError_t contig_dispatch(int logn, void* x, size_t batch, const void* 
   if constexpr (LO > HI) {
     return cudaErrorInvalidValue;
   } else {
-    if (logn == LO) return run_contig<W, LO, INV, GATHER>(x, batch, tw, p, norm, ga, s);
+    if (logn == LO) {
+      if constexpr (sizeof(W) == 8) {
+        if ((p & 0xffffffffull) == 1) return run_contig<W, LO, INV, GATHER, true>(x, batch, tw, p, norm, ga, s);
+      }
+      return run_contig<W, LO, INV, GATHER, false>(x, batch, tw, p, norm, ga, s);
+    }
     return contig_dispatch<W, INV, GATHER, LO + 1, HI>(logn, x, batch, tw, p, norm, ga, s);
   }
 }
@@ -544,7 +432,12 @@ static cudaError_t cols_dispatch(int logn, void* x, const ColsParams& prm, const
   if constexpr (LO > HI) {
     return cudaErrorInvalidValue;
   } else {
-    if (logn == LO) return run_cols<W, LO, INV>(x, prm, t, p, s);
+    if (logn == LO) {
+      if constexpr (sizeof(W) == 8) {
+        if ((p & 0xffffffffull) == 1) return run_cols<W, LO, INV, true>(x, prm, t, p, s);
+      }
+      return run_cols<W, LO, INV, false>(x, prm, t, p, s);
+    }
     return cols_dispatch<W, INV, LO + 1, HI>(logn, x, prm, t, p, s);
   }
 }
@@ -610,8 +503,12 @@ cudaError_t launch_calib(int wbytes, uint64_t p, uint64_t w, uint64_t wp, unsign
                          uint64_t* n_bfly, cudaStream_t s) {
   const unsigned grid = (unsigned)num_sms() * 8, th = 256;
   *n_bfly = (uint64_t)grid * th * 8 * iters;
-  if (wbytes == 8) k_calib<uint64_t><<<grid, th, 0, s>>>((uint64_t*)sink, p, w, wp, iters);
-  else k_calib<uint32_t><<<grid, th, 0, s>>>((uint32_t*)sink, (uint32_t)p, (uint32_t)w, (uint32_t)wp, iters);
+  if (wbytes == 8) {
+    if ((p & 0xffffffffull) == 1) k_calib<uint64_t, true><<<grid, th, 0, s>>>((uint64_t*)sink, p, w, wp, iters);
+    else k_calib<uint64_t, false><<<grid, th, 0, s>>>((uint64_t*)sink, p, w, wp, iters);
+  } else {
+    k_calib<uint32_t, false><<<grid, th, 0, s>>>((uint32_t*)sink, (uint32_t)p, (uint32_t)w, (uint32_t)wp, iters);
+  }
   return cudaGetLastError();
 }
 
@@ -620,12 +517,17 @@ cudaError_t launch_debug_bfly(int wbytes, int alg, const void* W, const void* Wp
   if (!n) return cudaSuccess;
   const int th = 256;
   const unsigned grid = (unsigned)((n + th - 1) / th);
-  if (wbytes == 8)
-    k_debug_bfly<uint64_t><<<grid, th, 0, s>>>(alg, (const uint64_t*)W, (const uint64_t*)Wp, (uint64_t*)X,
-                                                (uint64_t*)Y, n, p, J);
-  else
-    k_debug_bfly<uint32_t><<<grid, th, 0, s>>>(alg, (const uint32_t*)W, (const uint32_t*)Wp, (uint32_t*)X,
-                                                (uint32_t*)Y, n, (uint32_t)p, (uint32_t)J);
+  if (wbytes == 8) {
+    if ((p & 0xffffffffull) == 1)
+      k_debug_bfly<uint64_t, true><<<grid, th, 0, s>>>(alg, (const uint64_t*)W, (const uint64_t*)Wp, (uint64_t*)X,
+                                                        (uint64_t*)Y, n, p, J);
+    else
+      k_debug_bfly<uint64_t, false><<<grid, th, 0, s>>>(alg, (const uint64_t*)W, (const uint64_t*)Wp, (uint64_t*)X,
+                                                         (uint64_t*)Y, n, p, J);
+  } else {
+    k_debug_bfly<uint32_t, false><<<grid, th, 0, s>>>(alg, (const uint32_t*)W, (const uint32_t*)Wp, (uint32_t*)X,
+                                                       (uint32_t*)Y, n, (uint32_t)p, (uint32_t)J);
+  }
   return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -79,6 +80,32 @@ std::vector<uint8_t> make_table(uint64_t p, uint64_t root, uint64_t count, unsig
 }
 
 }  // namespace
+
+// Per-stage table of an N = 2^logn point transform with root `root` (rounds.cuh):
+// stage i (1-based) holds zeta_i^k = root^{2^{i-1} k}, k < N >> i, at offset N - (N >> (i-1)).
+// The first N/2 entries (stage 1) are root^e, e < N/2.
+std::vector<uint8_t> make_stage_table(uint64_t p, uint64_t root, unsigned logn, unsigned bits) {
+  const uint64_t N = (uint64_t)1 << logn;
+  std::vector<uint8_t> out;
+  if (logn == 0) return out;
+  out.reserve((N - 1) * 2 * (bits / 8));
+  uint64_t zeta = root;
+  for (unsigned i = 1; i <= logn; ++i) {
+    std::vector<uint8_t> t = make_table(p, zeta, N >> i, bits);
+    out.insert(out.end(), t.begin(), t.end());
+    zeta = mulmod(zeta, zeta, p);
+  }
+  return out;
+}
+
+bool tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NTT_DISABLE_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 struct ntt_plan_s {
   int device = 0;
@@ -179,7 +206,7 @@ ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out) {
   if (it != pl->extra_sub.end()) { *out = it->second; return NTT_OK; }
   const uint64_t L = (uint64_t)1 << pl->ell, Nn = (uint64_t)1 << logn;
   void* d = nullptr;
-  ntt_status st = upload(pl, make_table(pl->p, powmod(pl->omega, L / Nn, pl->p), Nn / 2, pl->bits), &d);
+  ntt_status st = upload(pl, make_stage_table(pl->p, powmod(pl->omega, L / Nn, pl->p), logn, pl->bits), &d);
   if (st != NTT_OK) return st;
   pl->extra_sub[logn] = d;
   *out = d;
@@ -278,9 +305,8 @@ ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned
   ntt_status st = NTT_OK;
   const unsigned bits = log2_beta;
   if (pl->passes.size() == 1) {
-    const uint64_t half = L / 2;
-    if ((st = upload(pl, make_table(p, omega, half, bits), &pl->tw_fwd)) != NTT_OK ||
-        (st = upload(pl, make_table(p, pl->omega_inv, half, bits), &pl->tw_inv)) != NTT_OK) {
+    if ((st = upload(pl, make_stage_table(p, omega, ell, bits), &pl->tw_fwd)) != NTT_OK ||
+        (st = upload(pl, make_stage_table(p, pl->omega_inv, ell, bits), &pl->tw_inv)) != NTT_OK) {
       free_plan(pl);
       return st;
     }
@@ -289,8 +315,8 @@ ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned
       const uint64_t Nn = (uint64_t)1 << n;
       const uint64_t rootN = powmod(omega, L / Nn, p), rootNi = powmod(pl->omega_inv, L / Nn, p);
       void *f = nullptr, *i = nullptr;
-      if ((st = upload(pl, make_table(p, rootN, Nn / 2, bits), &f)) != NTT_OK ||
-          (st = upload(pl, make_table(p, rootNi, Nn / 2, bits), &i)) != NTT_OK) {
+      if ((st = upload(pl, make_stage_table(p, rootN, n, bits), &f)) != NTT_OK ||
+          (st = upload(pl, make_stage_table(p, rootNi, n, bits), &i)) != NTT_OK) {
         free_plan(pl);
         return st;
       }
@@ -331,7 +357,7 @@ ntt_status ntt_plan_twiddles(ntt_plan_t pl, void* host_W, void* host_Wp) {
   if (pl->ell > 20) return NTT_ERR_UNSUPPORTED;
   const uint64_t half = ((uint64_t)1 << pl->ell) / 2;
   std::vector<uint8_t> t;
-  if (pl->tw_fwd) {  // the device table the kernels read
+  if (pl->tw_fwd) {  // the device table the kernels read (its stage-1 block is omega^e, e < L/2)
     DeviceGuard g(pl->device);
     t.resize(half * 2 * pl->wbytes);
     if (half) {
@@ -351,6 +377,15 @@ ntt_status ntt_plan_twiddles(ntt_plan_t pl, void* host_W, void* host_Wp) {
 
 static bool aligned16(const void* x) { return ((uintptr_t)x & 15) == 0; }
 
+// On-chip transform of `batch` contiguous N-point transforms: the TMA-staged
+// kernel where it applies (NTT_DISABLE_TMA=1 forces the register-direct one).
+static cudaError_t launch_contig_any(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
+                                     const void* tw, uint64_t p, cudaStream_t s) {
+  if (tma_enabled() && nttb::tma_supported(wbytes, logn))
+    return nttb::launch_contig_tma(wbytes, logn, inverse, normalize, x, batch, tw, p, s);
+  return nttb::launch_contig(wbytes, logn, inverse, normalize, x, batch, tw, p, s);
+}
+
 static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
   t_launches = 0;
   if (!pl || (!x && batch) || (x && !aligned16(x))) return NTT_ERR_ARG;
@@ -367,8 +402,8 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     return e == cudaSuccess ? NTT_OK : cuda_fail(e);
   }
   if (np == 1) {
-    e = nttb::launch_contig(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
-                            pl->p, s);
+    e = launch_contig_any(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
+                          pl->p, s);
     ++t_launches;
     return e == cudaSuccess ? NTT_OK : cuda_fail(e);
   }
@@ -399,12 +434,12 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     }
     if (e == cudaSuccess) {
       const size_t rows = batch * (L >> pl->passes[np - 1]);
-      e = nttb::launch_contig(pl->wbytes, (int)pl->passes[np - 1], false, true, x, rows, pl->sub_fwd[np - 1], pl->p, s);
+      e = launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], false, true, x, rows, pl->sub_fwd[np - 1], pl->p, s);
       ++t_launches;
     }
   } else {
     const size_t rows = batch * (L >> pl->passes[np - 1]);
-    e = nttb::launch_contig(pl->wbytes, (int)pl->passes[np - 1], true, false, x, rows, pl->sub_inv[np - 1], pl->p, s);
+    e = launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], true, false, x, rows, pl->sub_inv[np - 1], pl->p, s);
     ++t_launches;
     for (int j = (int)np - 2; j >= 0 && e == cudaSuccess; --j) {
       nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};

@@ -1,0 +1,146 @@
+// rounds.cuh -- the register "round" engine shared by every transform kernel.
+//
+// Algorithm 1 on an N = 2^LOGN point transform is cut into rounds of
+// SR <= LE consecutive stages.  In a round a thread holds G = E/2^SR groups of
+// 2^SR words; group (blk, c) holds positions blk*B + h*D + c (h < 2^SR) with
+// B = N >> LEVEL and D = N >> (LEVEL + SR), so all butterflies of the round's
+// stages pair words held by the same thread.
+//
+// Twiddles use the per-stage table layout: stage i (1-based) stores
+// zeta_i^k = omega^{2^{i-1} k} for k < m_i = N >> i at offset
+// N - (N >> (i-1)).  In every round the index k = hh*D + c is consecutive across
+// lanes (c) or uniform (D = 1), so table reads are coalesced / broadcast.
+#pragma once
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace nttb {
+
+template <class W> __device__ __forceinline__ void ldtw(const TwPair<W>* tw, uint32_t e, W& w, W& wp);
+template <> __device__ __forceinline__ void ldtw<uint64_t>(const TwPair<uint64_t>* tw, uint32_t e, uint64_t& w,
+                                                           uint64_t& wp) {
+  ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(tw) + e);
+  w = t.x;
+  wp = t.y;
+}
+template <> __device__ __forceinline__ void ldtw<uint32_t>(const TwPair<uint32_t>* tw, uint32_t e, uint32_t& w,
+                                                           uint32_t& wp) {
+  uint2 t = __ldg(reinterpret_cast<const uint2*>(tw) + e);
+  w = t.x;
+  wp = t.y;
+}
+
+// Offset of stage i's table inside the per-stage layout of an N-point transform.
+__host__ __device__ constexpr int stage_off(int logn, int i) { return (1 << logn) - ((1 << logn) >> (i - 1)); }
+
+// Round structure: R rounds of balanced stage counts sr(r) <= LE.
+template <int LOGN, int LE> struct Rounds {
+  static constexpr int R = (LOGN + LE - 1) / LE;
+  __host__ __device__ static constexpr int sr(int r) { return LOGN / R + (r < LOGN % R ? 1 : 0); }
+  __host__ __device__ static constexpr int level(int r) {
+    int s = 0;
+    for (int i = 0; i < r; ++i) s += sr(i);
+    return s;
+  }
+};
+
+// Forward round: stages LEVEL+1 .. LEVEL+SR with the Algorithm 3 butterfly; the
+// last stage of the transform (m = 1, all twiddles 1) uses the multiply-free path.
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
+__device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
+  constexpr int S = 1 << SR;
+  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
+#pragma unroll
+  for (int j = 0; j < SR; ++j) {
+    const int half = S >> (j + 1);
+    const bool w1 = (LEVEL + j + 1 == LOGN);
+    const int off = stage_off(LOGN, LEVEL + j + 1);
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+#pragma unroll
+      for (int hh = 0; hh < half; ++hh) {
+        W w = 1, wp = 0;
+        if (!w1) ldtw<W>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
+#pragma unroll
+        for (int b = 0; b < (1 << j); ++b) {
+          const int h = b * 2 * half + hh;
+          if (w1) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+          else bfly_alg3<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+        }
+      }
+    }
+  }
+}
+
+// Inverse round: the same stages run backwards, Algorithm 4 with the
+// inverse table zeta_i^{-k}.
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
+__device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, const Mod<W>& m) {
+  constexpr int S = 1 << SR;
+  constexpr int D = (1 << LOGN) >> (LEVEL + SR);
+#pragma unroll
+  for (int j = SR - 1; j >= 0; --j) {
+    const int half = S >> (j + 1);
+    const bool w1 = (LEVEL + j + 1 == LOGN);
+    const int off = stage_off(LOGN, LEVEL + j + 1);
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+#pragma unroll
+      for (int hh = 0; hh < half; ++hh) {
+        W w = 1, wp = 0;
+        if (!w1) ldtw<W>(twi, (uint32_t)(off + hh * D + c[q]), w, wp);
+#pragma unroll
+        for (int b = 0; b < (1 << j); ++b) {
+          const int h = b * 2 * half + hh;
+          if (w1) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+          else bfly_alg4<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+        }
+      }
+    }
+  }
+}
+
+// 16-byte vector helpers (two u64 or four u32 words).
+template <class W> __device__ __forceinline__ void unpack16(const uint4& u, W* v) {
+  if constexpr (sizeof(W) == 8) {
+    v[0] = ((uint64_t)u.y << 32) | u.x;
+    v[1] = ((uint64_t)u.w << 32) | u.z;
+  } else {
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  }
+}
+template <class W> __device__ __forceinline__ uint4 pack16(const W* v) {
+  uint4 u;
+  if constexpr (sizeof(W) == 8) {
+    u.x = (uint32_t)v[0]; u.y = (uint32_t)(v[0] >> 32);
+    u.z = (uint32_t)v[1]; u.w = (uint32_t)(v[1] >> 32);
+  } else {
+    u.x = v[0]; u.y = v[1]; u.z = v[2]; u.w = v[3];
+  }
+  return u;
+}
+
+// Contiguous run of S words: widest aligned vector accesses (global or shared).
+template <class W, int S> __device__ __forceinline__ void load_run(const W* src, W* v) {
+  if constexpr (S * sizeof(W) >= 16) {
+    constexpr int PER = 16 / sizeof(W);
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) unpack16<W>(*reinterpret_cast<const uint4*>(src + i * PER), v + i * PER);
+  } else {
+#pragma unroll
+    for (int i = 0; i < S; ++i) v[i] = src[i];
+  }
+}
+template <class W, int S> __device__ __forceinline__ void store_run(W* dst, const W* v) {
+  if constexpr (S * sizeof(W) >= 16) {
+    constexpr int PER = 16 / sizeof(W);
+#pragma unroll
+    for (int i = 0; i < S / PER; ++i) *reinterpret_cast<uint4*>(dst + i * PER) = pack16<W>(v + i * PER);
+  } else {
+#pragma unroll
+    for (int i = 0; i < S; ++i) dst[i] = v[i];
+  }
+}
+
+}  // namespace nttb
