@@ -57,6 +57,20 @@ def root(p, L):
     return pow(3, (p - 1) // L, p)
 
 
+def derived_alu_peak(bits, p, sms, clock_mhz):
+    """Butterflies/s bound of the fmaheavy (IMAD) pipe for Algorithm 3's multiplies (DESIGN.md
+    "Roofline").  Measured opcode rates per SM per clock (tools/int_pipe_peak.cu): IMAD.WIDE.U32 and
+    IMAD.HI 32, IMAD 64, i.e. 4 and 2 SMSP-cycles per warp instruction.
+      beta=2^64: hi64(W'T) 4 WIDE; lo64(WT) 1 WIDE + 2 IMAD; lo64(Qp) 1 WIDE + 2 IMAD
+                 -> 32 SMSP-cycles / warp-butterfly (26 when p = 1 mod 2^32: lo64(Qp) = 1 IMAD)
+      beta=2^32: Q 1 IMAD.HI; W*T - Q*p 2 IMAD -> 8 SMSP-cycles / warp-butterfly."""
+    if bits == 64:
+        cyc = 26 if (p & 0xFFFFFFFF) == 1 else 32
+    else:
+        cyc = 8
+    return sms * clock_mhz * 1e6 * 4 * 32 / cyc
+
+
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -191,7 +205,8 @@ def run_native(args, cfg, rank, world, local_rank):
         stream.synchronize()
         if it:
             calib.append(n / (e0.elapsed_time(e1) * 1e-3))
-    alu_peak = max(calib)
+    calib_peak = max(calib)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
     # ---- warmup
     for _ in range(args.warmup):
@@ -225,6 +240,8 @@ def run_native(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    clock_max = clocks.get("sm_max_mhz") or 1965.0
+    alu_peak = derived_alu_peak(bits, p0, sms, clock_max)
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -266,7 +283,9 @@ def run_native(args, cfg, rank, world, local_rank):
         "peak": round(alu_peak / 1e9, 2),
         "unit": "Gbutterflies/s",
         "frac": round(achieved_bfly / alu_peak, 4),
-        "peak_source": "live register-only Alg.3 butterfly loop (ntt_calibrate_butterfly), same process/clocks",
+        "peak_source": (f"derived fmaheavy-pipe bound of Alg.3's multiplies at {sms} SMs x {clock_max:.0f} MHz "
+                        "(DESIGN.md Roofline)"),
+        "calibrated_register_only_Gbfly_s": round(calib_peak / 1e9, 2),
         "traffic": traffic,
         "hbm": {"achieved_GBps": round(alg_bytes / (dom_ms * 1e-3) / 1e9, 1), "peak_GBps": hbm_peak,
                 "frac": round(alg_bytes / (dom_ms * 1e-3) / 1e9 / hbm_peak, 4),

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntt_b200.so")
+LIB_PATH = os.environ.get("NTT_B200_LIB") or os.path.join(_HERE, "libntt_b200.so")
 
 NTT_SCALE_INV_L = 1
 NTT_OP_FORWARD = 1

@@ -80,7 +80,10 @@ template <class W, int LOGN, int LE> struct TmaShape {
   static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E;
   static constexpr int K = T >= 256 ? 1 : 256 / T;   // transforms per tile
   static constexpr int THREADS = K * T;
-  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
+#ifndef NTT_TMA_MINB_THREADS
+#define NTT_TMA_MINB_THREADS 512
+#endif
+  static constexpr int MINB = THREADS >= NTT_TMA_MINB_THREADS ? 1 : NTT_TMA_MINB_THREADS / THREADS;
   static constexpr int TILE_WORDS = K * N;
   static constexpr int TILE_BYTES = TILE_WORDS * (int)sizeof(W);
   static constexpr int ROW_WORDS = 128 / (int)sizeof(W);
@@ -254,8 +257,14 @@ static int sm_count() {
   return n;
 }
 
+#ifndef NTT_TMA_LE64
+#define NTT_TMA_LE64 4
+#endif
+#ifndef NTT_TMA_LE32
+#define NTT_TMA_LE32 5
+#endif
 template <class W> struct TmaLE {
-  static constexpr int value = 4 + (sizeof(W) == 4 ? 1 : 0);
+  static constexpr int value = sizeof(W) == 8 ? NTT_TMA_LE64 : NTT_TMA_LE32;
 };
 
 template <class W, int LOGN, bool INV, bool PLO1>
