@@ -141,6 +141,7 @@ def run_native(args, cfg, rank, world, local_rank):
         batch //= world
     plans = [ntt.Plan(p, root(p, L), cfg["ell"], bits, device=local_rank) for p in cfg["primes"]]
     conv = cfg["ops"] == ("conv",)
+    dist_c5 = cfg["key"] == "c5" and world > 1  # one transform split four-step over the ranks
     # inputs generated in HBM by the seeded counter-based generator (synth/ definition)
     seed = 0x12052926 ^ cfg["seed_cfg"]
     first = rank * batch
@@ -157,6 +158,18 @@ def run_native(args, cfg, rank, world, local_rank):
             del tmp
             work = [(a0.clone(), b0.clone()) for _ in plans]
             src = (a0, b0)
+        elif dist_c5:
+            from paper_1205_2926_b200.dist import FourStepForward, FourStepLayout
+            lay = FourStepLayout(cfg["ell"], cfg["ell"] // 2, world)
+            full = torch.empty(L, dtype=dt, device=dev)  # the same global input on every rank
+            ntt.synth_uniform(full, seed, 0, bound=cfg["primes"][0], stream=stream)
+            c0, c1 = lay.columns(rank)
+            x0 = full.view(lay.N1, lay.N2)[:, c0:c1].contiguous().view(-1)
+            del full
+            x = x0.clone()
+            recv = torch.empty_like(x)
+            outbuf = torch.empty_like(x)
+            fs = FourStepForward(plans[0], lay, rank)
         else:
             x0 = torch.empty(batch * L, dtype=dt, device=dev)
             ntt.synth_uniform(x0, seed, 0, start=first * L, bound=cfg["primes"][0], stream=stream)
@@ -167,6 +180,16 @@ def run_native(args, cfg, rank, world, local_rank):
     def step(evs=None):
         """One step: the whole hot path over this rank's batch.  evs: events between launches."""
         launches = 0
+        if dist_c5:
+            with torch.cuda.stream(stream):
+                for name, fn in (("cols", lambda: fs.cols(x, stream)), ("all_to_all", lambda: fs.exchange(x, recv)),
+                                 ("rows", lambda: fs.rows(recv, outbuf, stream))):
+                    fn()
+                    launches += ntt.last_launch_count() if name != "all_to_all" else 0
+                    if evs is not None:
+                        evs.append((name, torch.cuda.Event(enable_timing=True)))
+                        evs[-1][1].record(stream)
+            return launches
         if conv:
             for pl, (a, b) in zip(plans, work):
                 pl.cyclic_convolve(a, b, stream=stream)
@@ -247,7 +270,7 @@ def run_native(args, cfg, rank, world, local_rank):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    bfly_rank = butterflies(cfg, batch)
+    bfly_rank = butterflies(cfg, batch) // (world if dist_c5 else 1)
     value = bfly_rank * world * args.steps / (total_ms * 1e-3)
 
     # ---- dominant kernel (largest share of the step) and its roofline
@@ -255,6 +278,8 @@ def run_native(args, cfg, rank, world, local_rank):
     dom = max(share, key=share.get)
     dom_ms = statistics.mean(kernel_ms[dom])
     per_launch_bfly = butterflies(cfg, batch) // (len(plans) if conv else len(cfg["ops"]))
+    if dist_c5:
+        per_launch_bfly = bfly_rank
     if conv:
         per_launch_bfly = butterflies(cfg, batch) // len(plans)  # one cyclic convolution (3 NTTs) per prime
     passes = plans[0].info().n_passes
@@ -296,7 +321,28 @@ def run_native(args, cfg, rank, world, local_rank):
     # ---- e2e: the same step through the C-ABI host-buffer call (ntt_execute_host),
     # H2D of the inputs and D2H of the results inside the timed region
     e2e = None
-    if not conv:
+    if dist_c5:
+        h_in = x0.cpu().pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        ms = []
+        for it in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            with torch.cuda.stream(stream):
+                x.copy_(h_in, non_blocking=True)
+                fs(x, recv, outbuf, stream)
+                h_out.copy_(outbuf, non_blocking=True)
+            e1.record(stream)
+            stream.synchronize()
+            if it:
+                ms.append(e0.elapsed_time(e1))
+        e2e_ms = sum(ms)
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": bfly_rank * world * len(ms) / (float(t.item()) * 1e-3), "unit": "butterflies/s",
+               "h2d_bytes_per_step": x.numel() * wb, "d2h_bytes_per_step": x.numel() * wb,
+               "api": "pinned shard copies + FourStepForward (cols, NCCL all_to_all_single, rows)"}
+    elif not conv:
         ops = 0
         for op in cfg["ops"]:
             ops |= ntt.NTT_OP_FORWARD if op == "fwd" else ntt.NTT_OP_INVERSE
@@ -352,11 +398,13 @@ def run_native(args, cfg, rank, world, local_rank):
         out = {
             "metric": METRIC, "value": value, "unit": "butterflies/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "u64" if bits == 64 else "u32",
+            "scaling": "strong" if dist_c5 else cfg["scaling"], "vs_baseline": None,
+            "dtype": "u64" if bits == 64 else "u32",
             "data": "synthetic: seeded counter-based uniform residues generated in HBM (synth/ definition)",
             "config": {"workload": cfg["workload"], "transforms_per_gpu": batch, "L": L,
                        "butterflies_per_step_per_gpu": bfly_rank,
-                       "parallelism": f"batch-sharded x{world}, no collective",
+                       "parallelism": (f"four-step split over {world} GPUs, one NCCL all_to_all" if dist_c5
+                                       else f"batch-sharded x{world}, no collective"),
                        "passes": passes,
                        "l2": "flushed between timed steps (256 MiB zero-fill, outside the step events)"},
             "hbm_GBps": round(2 * batch * L * wb * passes * (len(cfg['ops']) if not conv else 3 * len(plans))

@@ -565,7 +565,10 @@ ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned ran
   unsigned logC = 0;
   while ((1u << logC) < C) ++logC;
   DeviceGuard g(pl->device);
-  const uint64_t L = (uint64_t)1 << pl->ell;
+  {
+    ntt_status st = ensure_fourstep_tables(pl);  // before reading pl->H
+    if (st != NTT_OK) return st;
+  }
   cudaError_t e = cudaSuccess;
   unsigned outer = 0;
   for (unsigned j = 0; j < nc && e == cudaSuccess; ++j) {
@@ -587,7 +590,6 @@ ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned ran
     prm.col0 = rank << log_wl;
     void* subf = nullptr;
     ntt_status st = sub_table(pl, logN, &subf);
-    if (st == NTT_OK) st = ensure_fourstep_tables(pl);
     if (st != NTT_OK) return st;
     nttb::DevTables t{subf, subf, pl->fa, pl->fb};
     e = nttb::launch_cols(pl->wbytes, (int)logN, false, x, prm, t, pl->p, (cudaStream_t)stream);

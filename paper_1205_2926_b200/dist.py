@@ -1,0 +1,119 @@
+"""Multi-GPU partitioning of the NTT hot path.
+
+* Batched configs (C2-C4): independent transforms shard over ranks with no data-path collective
+  (`batch_shard`).
+* One oversized transform (C5): a four-step split.  View the length-L transform as an N1 x N2 row-major
+  matrix (N1 = 2^ell1).  Rank g of G holds the column shard c in [g N2/G, (g+1) N2/G) as an N1 x (N2/G)
+  row-major matrix and runs
+      ntt_fourstep_cols  (column NTTs of length N1 + twiddle omega^{c rev(r)}; stages 1..ell1 of Alg. 1,
+                          P:27-46, re-associated)
+      one all-to-all     (rank g sends rows [h N1/G, (h+1) N1/G) of its shard -- contiguous, no pack --
+                          to rank h)
+      ntt_fourstep_rows  (row NTTs of length N2 over the G received blocks, normalised)
+  and ends with flat positions [g L/G, (g+1) L/G) of Algorithm 1's bit-reversed output.
+
+The collective is `torch.distributed.all_to_all_single` on the NCCL process group (gloo in CPU tests);
+the compute steps are the CUDA kernels behind the C ABI (`Plan.fourstep_cols/rows`).  The layout
+helpers below are pure host logic, shared by the product path and the CPU tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def batch_shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [start, start+count) of `total` independent transforms for `rank`."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+@dataclass(frozen=True)
+class FourStepLayout:
+    """Shapes of the distributed four-step split of a length-2^ell transform over `world` ranks."""
+    ell: int
+    ell1: int
+    world: int
+
+    def __post_init__(self):
+        if self.world & (self.world - 1) or self.world < 1:
+            raise ValueError("world must be a power of two")
+        if not (0 < self.ell1 < self.ell):
+            raise ValueError("need 0 < ell1 < ell")
+        if self.N1 % self.world or self.N2 % self.world:
+            raise ValueError("world must divide N1 and N2")
+
+    @property
+    def N1(self) -> int:
+        return 1 << self.ell1
+
+    @property
+    def N2(self) -> int:
+        return 1 << (self.ell - self.ell1)
+
+    @property
+    def L(self) -> int:
+        return 1 << self.ell
+
+    @property
+    def local_width(self) -> int:          # columns per rank
+        return self.N2 // self.world
+
+    @property
+    def rows_per_rank(self) -> int:        # rows owned after the exchange
+        return self.N1 // self.world
+
+    @property
+    def shard_words(self) -> int:          # words per rank, before and after
+        return self.L // self.world
+
+    @property
+    def block_words(self) -> int:          # words per all-to-all block
+        return self.rows_per_rank * self.local_width
+
+    def columns(self, rank: int) -> tuple[int, int]:
+        """Global column range [c0, c1) held by `rank` before the exchange."""
+        return rank * self.local_width, (rank + 1) * self.local_width
+
+    def input_index(self, rank: int, r: int, c_local: int) -> int:
+        """Global (natural-order) input index of local element (r, c_local) of `rank`'s shard."""
+        return self.N2 * r + rank * self.local_width + c_local
+
+    def output_range(self, rank: int) -> tuple[int, int]:
+        """Flat positions of Algorithm 1's bit-reversed output held by `rank` after the rows pass."""
+        return rank * self.shard_words, (rank + 1) * self.shard_words
+
+
+def scatter_columns(x_flat, layout: FourStepLayout, rank: int):
+    """Host helper: `rank`'s column shard (N1 x N2/G, row-major) of a full natural-order input."""
+    c0, c1 = layout.columns(rank)
+    return x_flat.reshape(layout.N1, layout.N2)[:, c0:c1].reshape(-1)
+
+
+class FourStepForward:
+    """Distributed forward NTT of one length-2^ell transform (config C5) on the calling rank.
+
+    x_shard, recv, out: device tensors of layout.shard_words words each (recv/out may not alias x_shard).
+    """
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None):
+        self.plan, self.layout, self.rank, self.group = plan, layout, rank, group
+
+    def cols(self, x_shard, stream=None):
+        self.plan.fourstep_cols(self.layout.ell1, x_shard, self.rank, self.layout.world, stream=stream)
+
+    def exchange(self, x_shard, recv):
+        import torch.distributed as dist
+        if self.layout.world == 1:
+            recv.copy_(x_shard)
+        else:
+            dist.all_to_all_single(recv, x_shard, group=self.group)
+
+    def rows(self, recv, out, stream=None):
+        self.plan.fourstep_rows(self.layout.ell1, recv, out, self.rank, self.layout.world, stream=stream)
+
+    def __call__(self, x_shard, recv, out, stream=None):
+        self.cols(x_shard, stream)
+        self.exchange(x_shard, recv)
+        self.rows(recv, out, stream)
+        return out
