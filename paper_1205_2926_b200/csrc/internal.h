@@ -53,6 +53,11 @@ cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, vo
 bool tma_supported(int wbytes, int logn);
 cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
                               const void* tw, uint64_t p, cudaStream_t s);
+// transforms of length 2 * (on-chip max) on 2-CTA clusters (ntt_split2.cu); pw_a != nullptr
+// fuses the pointwise product a*b*L^{-1} into the inverse's load (cyclic convolution)
+bool split2_supported(int wbytes, int logn);
+cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
+                          const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s);
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
                         uint64_t p, cudaStream_t s);
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,

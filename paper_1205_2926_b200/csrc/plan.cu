@@ -187,11 +187,12 @@ void free_plan(ntt_plan_s* pl) {
 std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
   const unsigned cmax = wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
   const unsigned colmax = wbytes == 8 ? nttb::kColsMaxLog64 : nttb::kColsMaxLog32;
-  if (ell <= cmax) return {ell};
+  // the contiguous pass reaches 2 * (on-chip max) on a 2-CTA cluster (ntt_split2.cu)
+  if (ell <= cmax + 1) return {ell};
   for (unsigned np = 2;; ++np) {
     const unsigned col = std::min(colmax, ell / np);
     const unsigned last = ell - col * (np - 1);
-    if (last <= cmax) {
+    if (last <= cmax + 1) {
       std::vector<unsigned> s(np, col);
       s[np - 1] = last;
       return s;
@@ -381,6 +382,10 @@ static bool aligned16(const void* x) { return ((uintptr_t)x & 15) == 0; }
 // kernel where it applies (NTT_DISABLE_TMA=1 forces the register-direct one).
 static cudaError_t launch_contig_any(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
                                      const void* tw, uint64_t p, cudaStream_t s) {
+  if (nttb::split2_supported(wbytes, logn)) {  // always normalises; fine for every caller (A5)
+    (void)normalize;
+    return nttb::launch_split2(wbytes, logn, inverse, x, batch, tw, p, nullptr, nullptr, 0, 0, 0, s);
+  }
   if (tma_enabled() && nttb::tma_supported(wbytes, logn))
     return nttb::launch_contig_tma(wbytes, logn, inverse, normalize, x, batch, tw, p, s);
   return nttb::launch_contig(wbytes, logn, inverse, normalize, x, batch, tw, p, s);
@@ -540,6 +545,14 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, nt
   ntt_status st = ntt_forward(pl, a, batch, stream);
   total += t_launches;
   if (st == NTT_OK) { st = ntt_forward(pl, b, batch, stream); total += t_launches; }
+  if (st == NTT_OK && pl->passes.size() == 1 && nttb::split2_supported((int)pl->wbytes, (int)pl->ell)) {
+    // pointwise product (x L^{-1}) fused into the inverse's load
+    DeviceGuard g(pl->device);
+    cudaError_t e = nttb::launch_split2((int)pl->wbytes, (int)pl->ell, true, a, batch, pl->tw_inv, pl->p, a, b, pl->J,
+                                        pl->K_scale, pl->Kp_scale, (cudaStream_t)stream);
+    t_launches = total + 1;
+    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+  }
   if (st == NTT_OK) { st = ntt_pointwise_mul(pl, a, a, b, batch, NTT_SCALE_INV_L, stream); total += t_launches; }
   if (st == NTT_OK) { st = ntt_inverse(pl, a, batch, stream); total += t_launches; }
   t_launches = total;

@@ -45,8 +45,9 @@ template <int LOGN, int LE> struct Rounds {
   }
 };
 
-// Forward round: stages LEVEL+1 .. LEVEL+SR with the Algorithm 3 butterfly; the
-// last stage of the transform (m = 1, all twiddles 1) uses the multiply-free path.
+// Forward round: stages LEVEL+1 .. LEVEL+SR with the Algorithm 3 butterfly.
+// Butterflies known at compile time to have W = 1 (the whole last stage, m = 1, and
+// every k = 0 butterfly of a round with D = 1) take the multiply-free path.
 template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
   constexpr int S = 1 << SR;
@@ -60,12 +61,14 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
     for (int q = 0; q < G; ++q) {
 #pragma unroll
       for (int hh = 0; hh < half; ++hh) {
+        // k = hh*D + c; when D == 1 (c == 0) the hh == 0 butterflies have k = 0, i.e. W = 1
+        const bool unit = w1 || (D == 1 && hh == 0);
         W w = 1, wp = 0;
-        if (!w1) ldtw<W>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
+        if (!unit) ldtw<W>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (w1) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+          if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
           else bfly_alg3<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
         }
       }
@@ -88,12 +91,13 @@ __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* _
     for (int q = 0; q < G; ++q) {
 #pragma unroll
       for (int hh = 0; hh < half; ++hh) {
+        const bool unit = w1 || (D == 1 && hh == 0);  // k = 0: W = 1
         W w = 1, wp = 0;
-        if (!w1) ldtw<W>(twi, (uint32_t)(off + hh * D + c[q]), w, wp);
+        if (!unit) ldtw<W>(twi, (uint32_t)(off + hh * D + c[q]), w, wp);
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (w1) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+          if (unit) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
           else bfly_alg4<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
         }
       }

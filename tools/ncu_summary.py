@@ -93,7 +93,7 @@ def launches(csv_path, out_md):
         if len(r) <= vi or not r[vi]:
             continue
         v = float(r[vi].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki]
         short = name.split("(")[0]
         agg[short][0] += 1
