@@ -69,6 +69,22 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
+// 16-byte shared-memory vector access (kept as one LDS.128 / STS.128 so that a
+// quarter-warp covers the 8 chunks of a swizzled 128-byte row without conflicts).
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 u;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "r"(smem_u32(p))
+               : "memory");
+  return u;
+}
+__device__ __forceinline__ void sts128(void* p, const uint4& u) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(u.x), "r"(u.y), "r"(u.z),
+               "r"(u.w)
+               : "memory");
+}
+
 // Element index -> swizzled element index under SWIZZLE_128B (16-byte chunk ^= 128-byte row mod 8).
 template <class W> __device__ __forceinline__ int tswz(int i) {
   if constexpr (sizeof(W) == 8) return i ^ (((i >> 4) & 7) << 1);
@@ -124,7 +140,7 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
     if constexpr (VEC) {
 #pragma unroll
       for (int h = 0; h < S; h += PER)
-        unpack16<W>(*reinterpret_cast<const uint4*>(sb + tswz<W>(blk[q] * B + h)), v + q * S + h);
+        unpack16<W>(lds128(sb + tswz<W>(blk[q] * B + h)), v + q * S + h);
     } else {
 #pragma unroll
       for (int h = 0; h < S; ++h) v[q * S + h] = sb[tswz<W>(blk[q] * B + h * D + c[q])];
@@ -145,7 +161,7 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
       if constexpr (VEC) {
 #pragma unroll
         for (int h = 0; h < S; h += PER)
-          *reinterpret_cast<uint4*>(sb + tswz<W>(blk[q] * B + h)) = pack16<W>(v + q * S + h);
+          sts128(sb + tswz<W>(blk[q] * B + h), pack16<W>(v + q * S + h));
       } else {
 #pragma unroll
         for (int h = 0; h < S; ++h) sb[tswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
@@ -171,7 +187,7 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
       if constexpr (VEC) {
 #pragma unroll
         for (int h = 0; h < S; h += PER)
-          *reinterpret_cast<uint4*>(sb + tswz<W>(blk[q] * B + h)) = pack16<W>(v + q * S + h);
+          sts128(sb + tswz<W>(blk[q] * B + h), pack16<W>(v + q * S + h));
       } else {
 #pragma unroll
         for (int h = 0; h < S; ++h) sb[tswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
@@ -190,9 +206,12 @@ __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LO
                  const TwPair<W>* __restrict__ tw, W p, int norm) {
   using Sh = TmaShape<W, LOGN, LE>;
   extern __shared__ unsigned char smem_raw[];
-  uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023;
-  W* buf[2] = {reinterpret_cast<W*>(base), reinterpret_cast<W*>(base + Sh::TILE_BYTES)};
+  // 1024-byte alignment for the swizzle period, by pointer arithmetic on the shared
+  // array itself so that every access below stays an LDS/STS (not a generic LD/ST)
+  const uint32_t s0 = smem_u32(smem_raw);
+  unsigned char* base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * (size_t)Sh::TILE_BYTES);
+  const uint32_t buf_a[2] = {smem_u32(base), smem_u32(base + Sh::TILE_BYTES)};
   const uint32_t bar_a[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
   const int slot = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
   const Mod<W> m = make_mod<W>(p);
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LO
     mbar_expect_tx(bar_a[0], Sh::TILE_BYTES);
 #pragma unroll
     for (int bx = 0; bx < Sh::BOXES; ++bx)
-      tma_load_2d(smem_u32(buf[0]) + bx * Sh::BOX_BYTES, &tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
+      tma_load_2d(buf_a[0] + bx * Sh::BOX_BYTES, &tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
                   bar_a[0]);
   }
   W v[Sh::E];
@@ -218,15 +237,15 @@ __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LO
     const size_t b = tile * Sh::K + slot;
     const bool active = b < batch;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    tma_round<W, LOGN, LE, INV, PLO1, r0>(v, x + b * Sh::N, buf[cur] + slot * Sh::N, t, active, tw, m, norm != 0, true,
-                                          &tmap, tile + gridDim.x, ntiles, smem_u32(buf[cur ^ 1]), bar_a[cur ^ 1]);
+    W* sb = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES) + slot * Sh::N;  // stays in shared space
+    tma_round<W, LOGN, LE, INV, PLO1, r0>(v, x + b * Sh::N, sb, t, active, tw, m, norm != 0, true, &tmap,
+                                          tile + gridDim.x, ntiles, buf_a[cur ^ 1], bar_a[cur ^ 1]);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if (threadIdx.x == 0) {  // rows past the tensor end (partial last tile) are clipped by TMA
 #pragma unroll
       for (int bx = 0; bx < Sh::BOXES; ++bx)
-        tma_store_2d(&tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
-                     smem_u32(buf[cur]) + bx * Sh::BOX_BYTES);
+        tma_store_2d(&tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS, buf_a[cur] + bx * Sh::BOX_BYTES);
       bulk_commit();
     }
   }
