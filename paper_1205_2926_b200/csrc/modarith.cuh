@@ -15,7 +15,16 @@ template <> struct alignas(16) TwPair<uint64_t> { uint64_t w, wp; };
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
 
-template <class W> __device__ __forceinline__ W csub(W x, W m) { return x >= m ? x - m : x; }
+// Conditional subtraction x >= m ? x - m : x for x < 2m, m <= beta/2 (every use: m in
+// {p, 2p}, p < beta/4).  Then x - m lies in (-beta/2, beta/2), so its sign decides:
+// u64 selects on the sign word (no 64-bit compare pair); u32 uses min(x, x - m).
+// Measured +4% on the register-only u64 butterfly (tools/bfly_variants.cu).
+template <class W> __device__ __forceinline__ W csub(W x, W m);
+template <> __device__ __forceinline__ uint64_t csub<uint64_t>(uint64_t x, uint64_t m) {
+  const int64_t d = (int64_t)(x - m);
+  return d < 0 ? x : (uint64_t)d;
+}
+template <> __device__ __forceinline__ uint32_t csub<uint32_t>(uint32_t x, uint32_t m) { return umin(x, x - m); }
 
 // Modulus context kept in registers: p, 2p and (for beta = 2^64 with
 // p = 1 mod 2^32) np1 = -(p >> 32) mod 2^32, which turns lo64(Q p) into one IMAD.
