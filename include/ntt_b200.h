@@ -65,6 +65,19 @@ typedef enum {
 ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta, int device);
 ntt_status ntt_plan_destroy(ntt_plan_t plan);
 
+/* Same, with the forward butterfly selectable for the paper's own comparison (Table 1,
+ * P:212-228): NTT_BFLY_ALG3 = Algorithm 3 (default, the hot
+ * path), NTT_BFLY_ALG2 = Algorithm 2 (NTL, canonical operands; forward input must be
+ * < p), NTT_BFLY_ALG5 = Algorithm 5 (Montgomery; table holds W' = beta W mod p).
+ * ALG2/ALG5 plans support ntt_forward only for on-chip lengths 2^8..2^13 (beta=2^64) /
+ * 2^8..2^14 (beta=2^32); other calls return NTT_ERR_UNSUPPORTED.  ntt_inverse always
+ * uses Algorithm 4. */
+#define NTT_BFLY_ALG2 2u
+#define NTT_BFLY_ALG3 3u
+#define NTT_BFLY_ALG5 5u
+ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta,
+                              int device, unsigned butterfly);
+
 typedef struct {
   uint64_t p, omega, omega_inv, L_inv; /* L_inv = L^{-1} mod p */
   unsigned ell, log2_beta, word_bytes;

@@ -50,6 +50,7 @@ def _load() -> ctypes.CDLL:
     vp, u64, uint, sz, c_int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint, ctypes.c_size_t, ctypes.c_int
     sig = {
         "ntt_plan_create": [ctypes.POINTER(vp), u64, u64, uint, uint, c_int],
+        "ntt_plan_create_ex": [ctypes.POINTER(vp), u64, u64, uint, uint, c_int, uint],
         "ntt_plan_destroy": [vp],
         "ntt_plan_info": [vp, ctypes.POINTER(PlanInfo)],
         "ntt_forward": [vp, vp, sz, vp],
@@ -79,7 +80,7 @@ def _load() -> ctypes.CDLL:
 _lib = _load()
 
 EXPORTED = (
-    "ntt_plan_create", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_pointwise_mul",
+    "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_pointwise_mul",
     "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows", "ntt_synth_uniform",
     "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
 )
@@ -122,9 +123,11 @@ def last_launch_count() -> int:
 class Plan:
     """ntt_plan_create(p, omega, ell, log2_beta, device) (include/ntt_b200.h)."""
 
-    def __init__(self, p: int, omega: int, ell: int, log2_beta: int, device: int = 0):
+    def __init__(self, p: int, omega: int, ell: int, log2_beta: int, device: int = 0, butterfly: int = 3):
         h = ctypes.c_void_p()
-        _check(_lib.ntt_plan_create(ctypes.byref(h), p, omega, ell, log2_beta, device), "ntt_plan_create")
+        _check(_lib.ntt_plan_create_ex(ctypes.byref(h), p, omega, ell, log2_beta, device, butterfly),
+               "ntt_plan_create_ex")
+        self.butterfly = butterfly
         self._h = h
         self.p, self.omega, self.ell, self.log2_beta, self.device = p, omega, ell, log2_beta, device
         self.L = 1 << ell

@@ -51,8 +51,9 @@ struct DevTables {
 cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch, const void* tw,
                           uint64_t p, cudaStream_t s);
 bool tma_supported(int wbytes, int logn);
+// bf: forward butterfly 3 (Algorithm 3), 2 (Algorithm 2) or 5 (Algorithm 5) -- F1/F2 ablations
 cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
-                              const void* tw, uint64_t p, cudaStream_t s);
+                              const void* tw, uint64_t p, cudaStream_t s, int bf = 3);
 // transforms of length 2 * (on-chip max) on 2-CTA clusters (ntt_split2.cu); pw_a != nullptr
 // fuses the pointwise product a*b*L^{-1} into the inverse's load (cyclic convolution)
 bool split2_supported(int wbytes, int logn);

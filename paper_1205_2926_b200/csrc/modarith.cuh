@@ -31,12 +31,17 @@ template <> __device__ __forceinline__ uint32_t csub<uint32_t>(uint32_t x, uint3
 template <class W> struct Mod {
   W p, p2;
   uint32_t np1;
+  W J;  // p^{-1} mod beta (Algorithm 5 only)
 };
 template <class W> __device__ __forceinline__ Mod<W> make_mod(W p) {
   Mod<W> m;
   m.p = p;
   m.p2 = 2 * p;
   m.np1 = (uint32_t)(0u - (uint32_t)((uint64_t)p >> 32));
+  W j = p;  // Newton: 3 correct bits for odd p, doubling each step
+#pragma unroll
+  for (int i = 0; i < 6; ++i) j *= (W)2 - p * j;
+  m.J = j;
   return m;
 }
 
@@ -76,7 +81,7 @@ __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, const Mod<W>& m
   X = s;
 }
 template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, W p, W p2) {
-  bfly_alg3<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u});
+  bfly_alg3<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u, 0});
 }
 
 // W = 1 butterflies (O(L) butterflies have W = 1 and are cheaper):
@@ -98,7 +103,7 @@ __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, const Mod<W>& m
   Y = x - T + m.p2;
 }
 template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, W p, W p2) {
-  bfly_alg4<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u});
+  bfly_alg4<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u, 0});
 }
 
 // W = 1 inverse butterfly: T = Y reduced once by 2p (Y < 4p -> T < 2p).
@@ -117,6 +122,20 @@ template <class W> __device__ __forceinline__ void bfly_alg2(W& X, W& Y, W w, W 
   W r = csub<W>(shoup_mul<W>(T, w, wp, p), p);
   X = s;
   Y = r;
+}
+
+// Algorithm 2 inside the transform kernels (ablation F1), same Shoup core as Alg. 3.
+template <class W, bool PLO1>
+__device__ __forceinline__ void bfly_alg2m(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  W s = csub<W>(X + Y, m.p);                        // lines 1-2
+  W T = (X < Y) ? X - Y + m.p : X - Y;               // lines 3-4 (X < Y realises T < 0)
+  Y = csub<W>(shoup_mul<W, PLO1>(T, w, wp, m), m.p);  // lines 5-7
+  X = s;
+}
+template <class W> __device__ __forceinline__ void bfly_alg2_w1(W& X, W& Y, W p) {
+  W s = csub<W>(X + Y, p);
+  Y = (X < Y) ? X - Y + p : X - Y;
+  X = s;
 }
 
 // Full product hi/lo for Algorithm 5.
@@ -141,6 +160,10 @@ template <class W> __device__ __forceinline__ void bfly_alg5(W& X, W& Y, W wm, W
   W H = mulhi(Q, p);        // line 6
   Y = R1 - H + p;           // line 7
   X = s;
+}
+
+template <class W> __device__ __forceinline__ void bfly_alg5m(W& X, W& Y, W wm, const Mod<W>& m) {
+  bfly_alg5<W>(X, Y, wm, m.J, m.p, m.p2);
 }
 
 // Final normalisation: [0,2p) -> [0,p) and [0,4p) -> [0,p).

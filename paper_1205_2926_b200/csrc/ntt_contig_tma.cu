@@ -114,7 +114,7 @@ template <class W, int LOGN, int LE> struct TmaShape {
   static_assert(N * sizeof(W) % 1024 == 0, "slot buffers must keep the 1024-byte swizzle period");
 };
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int BF, int r>
 __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t, bool active,
                                           const TwPair<W>* __restrict__ tw, const Mod<W>& m, bool norm,
                                           bool first_exchange, const CUtensorMap* map, size_t next_tile,
@@ -147,7 +147,7 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
     }
   }
   // ---- compute
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF>(v, c, tw, m);
   else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (last) {
     if (norm) {
@@ -195,12 +195,12 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
     }
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    tma_round<W, LOGN, LE, INV, PLO1, nr>(v, xb, sb, t, active, tw, m, norm, false, map, next_tile, ntiles, next_buf,
-                                          next_bar);
+    tma_round<W, LOGN, LE, INV, PLO1, BF, nr>(v, xb, sb, t, active, tw, m, norm, false, map, next_tile, ntiles,
+                                              next_buf, next_bar);
   }
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int BF>
 __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LOGN, LE>::MINB)
     k_contig_tma(const __grid_constant__ CUtensorMap tmap, W* __restrict__ x, size_t batch,
                  const TwPair<W>* __restrict__ tw, W p, int norm) {
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LO
     const bool active = b < batch;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
     W* sb = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES) + slot * Sh::N;  // stays in shared space
-    tma_round<W, LOGN, LE, INV, PLO1, r0>(v, x + b * Sh::N, sb, t, active, tw, m, norm != 0, true, &tmap,
-                                          tile + gridDim.x, ntiles, buf_a[cur ^ 1], bar_a[cur ^ 1]);
+    tma_round<W, LOGN, LE, INV, PLO1, BF, r0>(v, x + b * Sh::N, sb, t, active, tw, m, norm != 0, true, &tmap,
+                                              tile + gridDim.x, ntiles, buf_a[cur ^ 1], bar_a[cur ^ 1]);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if (threadIdx.x == 0) {  // rows past the tensor end (partial last tile) are clipped by TMA
@@ -286,7 +286,7 @@ template <class W> struct TmaLE {
   static constexpr int value = sizeof(W) == 8 ? NTT_TMA_LE64 : NTT_TMA_LE32;
 };
 
-template <class W, int LOGN, bool INV, bool PLO1>
+template <class W, int LOGN, bool INV, bool PLO1, int BF>
 static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bool norm, cudaStream_t s) {
   constexpr int LE = TmaLE<W>::value;
   using Sh = TmaShape<W, LOGN, LE>;
@@ -302,7 +302,7 @@ static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bo
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto kern = k_contig_tma<W, LOGN, LE, INV, PLO1>;
+  auto kern = k_contig_tma<W, LOGN, LE, INV, PLO1, BF>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
@@ -318,19 +318,19 @@ static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bo
   return cudaGetLastError();
 }
 
-template <class W, bool INV, int LO, int HI>
+template <class W, bool INV, int BF, int LO, int HI>
 static cudaError_t tma_dispatch(int logn, void* x, size_t batch, const void* tw, uint64_t p, bool norm,
                                 cudaStream_t s) {
   if constexpr (LO > HI) {
     return cudaErrorInvalidValue;
   } else {
     if (logn == LO) {
-      if constexpr (sizeof(W) == 8) {
-        if ((p & 0xffffffffull) == 1) return run_tma<W, LO, INV, true>(x, batch, tw, p, norm, s);
+      if constexpr (sizeof(W) == 8 && BF != 5) {
+        if ((p & 0xffffffffull) == 1) return run_tma<W, LO, INV, true, BF>(x, batch, tw, p, norm, s);
       }
-      return run_tma<W, LO, INV, false>(x, batch, tw, p, norm, s);
+      return run_tma<W, LO, INV, false, BF>(x, batch, tw, p, norm, s);
     }
-    return tma_dispatch<W, INV, LO + 1, HI>(logn, x, batch, tw, p, norm, s);
+    return tma_dispatch<W, INV, BF, LO + 1, HI>(logn, x, batch, tw, p, norm, s);
   }
 }
 
@@ -339,12 +339,19 @@ bool tma_supported(int wbytes, int logn) {
 }
 
 cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch,
-                              const void* tw, uint64_t p, cudaStream_t s) {
-  if (wbytes == 8)
-    return inverse ? tma_dispatch<uint64_t, true, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s)
-                   : tma_dispatch<uint64_t, false, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
-  return inverse ? tma_dispatch<uint32_t, true, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s)
-                 : tma_dispatch<uint32_t, false, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
+                              const void* tw, uint64_t p, cudaStream_t s, int bf) {
+  if (inverse) {
+    if (wbytes == 8) return tma_dispatch<uint64_t, true, 3, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
+    return tma_dispatch<uint32_t, true, 3, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
+  }
+  if (wbytes == 8) {
+    if (bf == 2) return tma_dispatch<uint64_t, false, 2, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
+    if (bf == 5) return tma_dispatch<uint64_t, false, 5, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
+    return tma_dispatch<uint64_t, false, 3, kTmaMinLog, kTmaMaxLog64>(logn, x, batch, tw, p, normalize, s);
+  }
+  if (bf == 2) return tma_dispatch<uint32_t, false, 2, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
+  if (bf == 5) return tma_dispatch<uint32_t, false, 5, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
+  return tma_dispatch<uint32_t, false, 3, kTmaMinLog, kTmaMaxLog32>(logn, x, batch, tw, p, normalize, s);
 }
 
 }  // namespace nttb

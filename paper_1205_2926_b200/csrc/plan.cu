@@ -98,6 +98,22 @@ std::vector<uint8_t> make_stage_table(uint64_t p, uint64_t root, unsigned logn, 
   return out;
 }
 
+// Algorithm 5 variant of the per-stage table: first word W'_mont = beta * W mod p,
+// second word unused.
+std::vector<uint8_t> make_stage_table_mont(uint64_t p, uint64_t root, unsigned logn, unsigned bits) {
+  std::vector<uint8_t> t = make_stage_table(p, root, logn, bits);
+  const size_t wb = bits / 8, n = t.size() / (2 * wb);
+  const uint64_t bmodp = (uint64_t)(((u128)1 << bits) % p);
+  for (size_t e = 0; e < n; ++e) {
+    uint64_t w = 0;
+    memcpy(&w, &t[2 * e * wb], wb);
+    const uint64_t wm = mulmod(w, bmodp, p), zero = 0;
+    memcpy(&t[2 * e * wb], &wm, wb);
+    memcpy(&t[(2 * e + 1) * wb], &zero, wb);
+  }
+  return t;
+}
+
 bool tma_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -111,6 +127,7 @@ struct ntt_plan_s {
   int device = 0;
   uint64_t p = 0, omega = 0, omega_inv = 0, L_inv = 0, J = 0;
   unsigned ell = 0, bits = 0, wbytes = 0;
+  unsigned bfly = 3;  // forward butterfly (NTT_BFLY_ALG*)
   // schedule: log2 sub-lengths of the passes, outermost first
   std::vector<unsigned> passes;
   // device tables
@@ -262,7 +279,13 @@ const char* ntt_last_cuda_error(void) { return t_cuda_err; }
 unsigned ntt_last_launch_count(void) { return t_launches; }
 
 ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta, int device) {
+  return ntt_plan_create_ex(out, p, omega, ell, log2_beta, device, NTT_BFLY_ALG3);
+}
+
+ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned ell, unsigned log2_beta,
+                              int device, unsigned butterfly) {
   if (!out) return NTT_ERR_ARG;
+  if (butterfly != NTT_BFLY_ALG2 && butterfly != NTT_BFLY_ALG3 && butterfly != NTT_BFLY_ALG5) return NTT_ERR_ARG;
   *out = nullptr;
   if (log2_beta != 32 && log2_beta != 64) return NTT_ERR_WORD;
   // P:114 / P:146: p < beta/4; p odd prime ("word-sized prime", Alg. 5 "p odd")
@@ -287,6 +310,7 @@ ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned
   pl->ell = ell;
   pl->bits = log2_beta;
   pl->wbytes = log2_beta / 8;
+  pl->bfly = butterfly;
   {
     // J = p^{-1} mod beta by Newton iteration
     uint64_t j = p;  // correct to 3 bits for odd p
@@ -306,7 +330,9 @@ ntt_status ntt_plan_create(ntt_plan_t* out, uint64_t p, uint64_t omega, unsigned
   ntt_status st = NTT_OK;
   const unsigned bits = log2_beta;
   if (pl->passes.size() == 1) {
-    if ((st = upload(pl, make_stage_table(p, omega, ell, bits), &pl->tw_fwd)) != NTT_OK ||
+    if ((st = upload(pl, butterfly == NTT_BFLY_ALG5 ? make_stage_table_mont(p, omega, ell, bits)
+                                                    : make_stage_table(p, omega, ell, bits),
+                     &pl->tw_fwd)) != NTT_OK ||
         (st = upload(pl, make_stage_table(p, pl->omega_inv, ell, bits), &pl->tw_inv)) != NTT_OK) {
       free_plan(pl);
       return st;
@@ -403,6 +429,12 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
   const unsigned np = (unsigned)pl->passes.size();
   if (pl->ell == 0) {  // identity; only the normalisation remains
     e = nttb::launch_normalize(pl->wbytes, x, batch, pl->p, inverse ? 1 : 0, s);
+    ++t_launches;
+    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+  }
+  if (pl->bfly != NTT_BFLY_ALG3 && !inverse) {  // F1/F2 ablation: on-chip TMA kernel only
+    if (np != 1 || !nttb::tma_supported((int)pl->wbytes, (int)pl->ell)) return NTT_ERR_UNSUPPORTED;
+    e = nttb::launch_contig_tma(pl->wbytes, (int)pl->ell, false, true, x, batch, pl->tw_fwd, pl->p, s, (int)pl->bfly);
     ++t_launches;
     return e == cudaSuccess ? NTT_OK : cuda_fail(e);
   }

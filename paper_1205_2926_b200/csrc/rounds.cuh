@@ -48,7 +48,10 @@ template <int LOGN, int LE> struct Rounds {
 // Forward round: stages LEVEL+1 .. LEVEL+SR with the Algorithm 3 butterfly.
 // Butterflies known at compile time to have W = 1 (the whole last stage, m = 1, and
 // every k = 0 butterfly of a round with D = 1) take the multiply-free path.
-template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
+// BF selects the butterfly: 3 = Algorithm 3 (the product path), 2 = Algorithm 2 and
+// 5 = Algorithm 5 (ablations F1/F2 of SURVEY.md §8(f); Alg. 5 reads W' = beta W mod p
+// from the first word of each table pair).
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
   constexpr int S = 1 << SR;
   constexpr int D = (1 << LOGN) >> (LEVEL + SR);
@@ -68,8 +71,16 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
-          else bfly_alg3<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          if constexpr (BF == 2) {
+            if (unit) bfly_alg2_w1<W>(v[q * S + h], v[q * S + h + half], m.p);
+            else bfly_alg2m<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          } else if constexpr (BF == 5) {
+            if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+            else bfly_alg5m<W>(v[q * S + h], v[q * S + h + half], w, m);
+          } else {
+            if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
+            else bfly_alg3<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          }
         }
       }
     }

@@ -4,6 +4,7 @@ import numpy as np
 P30 = 998244353                    # 119*2^23 + 1 (configs C1, C3)
 P62 = 29 * 2**57 + 1               # configs C2, C4, C5
 RNS = (469762049, 167772161, 998244353)
+P62G = 2305843009146585089        # 62-bit, 2^24 | p-1, p != 1 mod 2^32: exercises the generic u64 Shoup tail
 
 
 def root(p, L):

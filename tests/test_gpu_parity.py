@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 import oracle  # noqa: E402
 import synth  # noqa: E402
-from gpu_util import P30, P62, RNS, bitrev, rand_residues, root, to_dev, to_host  # noqa: E402
+from gpu_util import P30, P62, P62G, RNS, bitrev, rand_residues, root, to_dev, to_host  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -70,6 +70,12 @@ def test_single_pass_u64(ntt, ell):
 ])
 def test_multi_pass(ntt, p, bits, ell, batch):
     _roundtrip_case(ntt, p, bits, ell, batch, seed=ell * 7 + bits, top=True)
+
+
+@pytest.mark.parametrize("ell,batch", [(4, 9), (9, 7), (12, 5), (13, 3), (14, 2), (15, 2), (16, 1), (20, 1), (24, 1)])
+def test_generic_u64_prime(ntt, ell, batch):
+    """p = 2305843009146585089 (not 1 mod 2^32): the generic lo64(Qp) path of every kernel."""
+    _roundtrip_case(ntt, P62G, 64, ell, batch, seed=500 + ell, top=True)
 
 
 def test_cross_width_identity(ntt):
@@ -142,7 +148,6 @@ def test_config3_rns_convolution(ntt):
     L = 1 << ell
     a = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
     b = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
-    ntt.synth_uniform(a[:, :half].contiguous().view(-1), synth.config_seed(3), 0, bits=20)  # layout check below
     ah = synth.uniform_bits(synth.config_seed(3), 0, 0, npairs * half, 20).reshape(npairs, half)
     bh = synth.uniform_bits(synth.config_seed(3), 1, 0, npairs * half, 20).reshape(npairs, half)
     a[:, :half] = torch.from_numpy(ah.astype(np.uint32)).cuda()
