@@ -147,6 +147,44 @@ ntt_status ntt_fourstep_cols(ntt_plan_t plan, unsigned ell1, void* x_shard, unsi
 ntt_status ntt_fourstep_rows(ntt_plan_t plan, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,
                              ntt_stream_t stream);
 
+/* ---- the same split run backwards, and layout helpers ----
+ *   ntt_fourstep_rows_inv: `in` holds this rank's N1/G rows of Algorithm 1's
+ *     bit-reversed output (flat positions [g L/G, (g+1) L/G), i.e. what
+ *     ntt_fourstep_rows wrote), each in [0,4p).  Runs the inverse (Algorithm 1
+ *     backwards, Algorithm 4 butterfly) of length N2 on every row (root
+ *     omega^{-N1}), natural order out, and writes row r's columns
+ *     [h N2/G, (h+1) N2/G) to block h of `send` (G blocks of (N1/G) x (N2/G) words,
+ *     row-major, back to back): the all-to-all send layout.  `in` is not modified;
+ *     `send` must not alias it.
+ *   ntt_fourstep_cols_inv: after the all-to-all, x_shard is this rank's column
+ *     shard (N1 x N2/G, row-major).  Multiplies M[r][c] by omega^{-c rev_{ell1}(r)}
+ *     then runs inverse NTTs of length N1 down every local column (root
+ *     omega^{-N2}); output normalised to [0,p), natural order: the column shard of
+ *     L*a when the spectrum was ntt_forward(a) (unscaled, like ntt_inverse).
+ * Same size constraints as ntt_fourstep_cols / ntt_fourstep_rows. */
+ntt_status ntt_fourstep_rows_inv(ntt_plan_t plan, unsigned ell1, const void* in, void* send, unsigned rank,
+                                 unsigned world, ntt_stream_t stream);
+ntt_status ntt_fourstep_cols_inv(ntt_plan_t plan, unsigned ell1, void* x_shard, unsigned rank, unsigned world,
+                                 ntt_stream_t stream);
+
+/* Block transpose dst[j][i][k] = src[i][j][k] for i < n0, j < n1, k < n2 (words of
+ * word_bytes = 4 or 8; device buffers, 16-byte aligned, not aliasing).  The pack /
+ * unpack between a contiguous shard (rows of N2 words) and the all-to-all block
+ * layout for the contiguous-input / contiguous-output distributed transforms
+ * (n0 = N1/G rows, n1 = G blocks, n2 = N2/G words, or n0 and n1 swapped). */
+ntt_status ntt_block_transpose(void* dst, const void* src, size_t n0, size_t n1, size_t n2, unsigned word_bytes,
+                               ntt_stream_t stream);
+
+/* Three-prime CRT (the RNS use of P:21): for i < n,
+ * out[2i] + 2^64 out[2i+1] = the unique x in [0, p0 p1 p2) with x = r_k[i] mod p_k
+ * (Garner's mixed-radix form, every constant multiply a Shoup multiply).
+ * p0, p1, p2: distinct odd primes < 2^30; r_k: device arrays of n canonical residues
+ * (uint32_t, < p_k, not checked); out: device array of 2n uint64_t, 16-byte aligned.
+ * With the residues of a three-prime cyclic convolution (config C3) whose true
+ * coefficients are < p0 p1 p2, out is the exact integer product. */
+ntt_status ntt_crt3(uint64_t* out, const uint32_t* r0, const uint32_t* r1, const uint32_t* r2, size_t n, uint32_t p0,
+                    uint32_t p1, uint32_t p2, ntt_stream_t stream);
+
 /* Seeded counter-based generator (test/bench infrastructure; same definition as
  * synth/__init__.py): x[i] = element (start+i) of stream (seed, tensor_id),
  * uniform in [0, bound) by rejection if bound != 0, else uniform in [0, 2^bits).

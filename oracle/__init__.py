@@ -163,3 +163,19 @@ def bfly(alg: int, bb: int, p: int, W, Wp, X, Y, J: int = 0):
     if rc:
         raise ValueError(f"unknown butterfly algorithm {alg}")
     return Xo, Yo
+
+
+def crt(residues, primes):
+    """The plain definition behind F3 (RNS use): for each index, the unique integer x in
+    [0, prod(primes)) with x = residues[k] mod primes[k], by the textbook CRT formula
+    x = sum_k r_k M_k (M_k^{-1} mod p_k) mod M, M_k = M / p_k, in Python integers.
+    Returns a list of Python ints."""
+    M = 1
+    for q in primes:
+        M *= q
+    terms = []
+    for q in primes:
+        Mk = M // q
+        terms.append(Mk * pow(Mk % q, -1, q))
+    cols = [np.asarray(r, dtype=np.uint64).reshape(-1) for r in residues]
+    return [sum(int(c[i]) * t for c, t in zip(cols, terms)) % M for i in range(cols[0].size)]

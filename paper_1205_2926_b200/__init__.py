@@ -60,6 +60,10 @@ def _load() -> ctypes.CDLL:
         "ntt_plan_twiddles": [vp, vp, vp],
         "ntt_fourstep_cols": [vp, uint, vp, uint, uint, vp],
         "ntt_fourstep_rows": [vp, uint, vp, vp, uint, uint, vp],
+        "ntt_fourstep_cols_inv": [vp, uint, vp, uint, uint, vp],
+        "ntt_fourstep_rows_inv": [vp, uint, vp, vp, uint, uint, vp],
+        "ntt_block_transpose": [vp, vp, sz, sz, sz, uint, vp],
+        "ntt_crt3": [vp, vp, vp, vp, sz, uint, uint, uint, vp],
         "ntt_synth_uniform": [vp, sz, uint, u64, u64, u64, u64, uint, vp],
         "ntt_debug_butterfly": [vp, c_int, vp, vp, vp, vp, sz, vp],
         "ntt_execute_host": [vp, uint, vp, vp, sz, vp, sz, vp],
@@ -81,7 +85,8 @@ _lib = _load()
 
 EXPORTED = (
     "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_pointwise_mul",
-    "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows", "ntt_synth_uniform",
+    "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
+    "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
     "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
 )
 
@@ -205,6 +210,14 @@ class Plan:
         _check(_lib.ntt_fourstep_rows(self._h, ell1, _ptr(recv), _ptr(out), rank, world, _stream(stream)),
                "ntt_fourstep_rows")
 
+    def fourstep_rows_inv(self, ell1, x_rows, send, rank, world, stream=None):
+        _check(_lib.ntt_fourstep_rows_inv(self._h, ell1, _ptr(x_rows), _ptr(send), rank, world, _stream(stream)),
+               "ntt_fourstep_rows_inv")
+
+    def fourstep_cols_inv(self, ell1, x_shard, rank, world, stream=None):
+        _check(_lib.ntt_fourstep_cols_inv(self._h, ell1, _ptr(x_shard), rank, world, _stream(stream)),
+               "ntt_fourstep_cols_inv")
+
     def debug_butterfly(self, alg, W, Wp, X, Y, stream=None):
         _check(_lib.ntt_debug_butterfly(self._h, alg, _ptr(W), _ptr(Wp), _ptr(X), _ptr(Y), X.numel(),
                                         _stream(stream)), "ntt_debug_butterfly")
@@ -216,6 +229,23 @@ def calibrate_butterfly(log2_beta: int, p: int, W: int, Wp: int, iters: int, sin
     _check(_lib.ntt_calibrate_butterfly(log2_beta, p, W, Wp, iters, _ptr(sink), ctypes.byref(n), _stream(stream)),
            "ntt_calibrate_butterfly")
     return int(n.value)
+
+
+def block_transpose(dst, src, n0: int, n1: int, n2: int, stream=None):
+    """ntt_block_transpose: dst[j][i][k] = src[i][j][k] (device tensors of 4- or 8-byte words)."""
+    _check(_lib.ntt_block_transpose(_ptr(dst), _ptr(src), n0, n1, n2, src.element_size(), _stream(stream)),
+           "ntt_block_transpose")
+    return dst
+
+
+def crt3(out, r0, r1, r2, primes, stream=None):
+    """ntt_crt3: out (uint64 device tensor of 2n words: lo, hi per coefficient) = the CRT lift of the
+    three uint32 residue tensors r0, r1, r2 (n words each) modulo primes = (p0, p1, p2)."""
+    n = r0.numel()
+    if r1.numel() != n or r2.numel() != n or out.numel() < 2 * n:
+        raise ValueError("crt3: size mismatch")
+    _check(_lib.ntt_crt3(_ptr(out), _ptr(r0), _ptr(r1), _ptr(r2), n, *primes, _stream(stream)), "ntt_crt3")
+    return out
 
 
 def synth_uniform(x, seed: int, tensor_id: int, start: int = 0, bound: int = 0, bits: int = 0, stream=None):

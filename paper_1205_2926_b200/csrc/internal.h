@@ -63,6 +63,22 @@ cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsP
                         uint64_t p, cudaStream_t s);
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
                                uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s);
+// distributed inverse (F4): inverse row NTTs, natural-order rows scattered into the send blocks
+cudaError_t launch_rows_scatter(int wbytes, int logn2, const void* in, void* send, uint32_t log_rows_local,
+                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s);
+cudaError_t launch_block_transpose(int wbytes, void* dst, const void* src, uint64_t n0, uint64_t n1, uint64_t n2,
+                                   cudaStream_t s);
+// three-prime CRT (Garner), constants precomputed on the host (plan.cu, ntt_crt3)
+struct Crt3Consts {
+  uint32_t p0, p1, p2;
+  uint32_t c01, c01p;  // p0^{-1} mod p1 and its Shoup W' (beta = 2^32)
+  uint32_t c02, c02p;  // p0^{-1} mod p2
+  uint32_t c12, c12p;  // p1^{-1} mod p2
+  uint32_t K1, K2, K3; // multiples of p1, p2, p2 that keep the Shoup inputs non-negative
+  uint64_t p01;        // p0 p1
+};
+cudaError_t launch_crt3(uint64_t* out, const uint32_t* r0, const uint32_t* r1, const uint32_t* r2, size_t n,
+                        const Crt3Consts& k, cudaStream_t s);
 cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, size_t n, uint64_t p, uint64_t J,
                              uint64_t K, uint64_t Kp, cudaStream_t s);
 cudaError_t launch_normalize(int wbytes, void* x, size_t n, uint64_t p, int from4p, cudaStream_t s);

@@ -40,9 +40,11 @@ template <int LOGN, int LE> struct ContigShape {
   static constexpr int R = RC::R;
 };
 
+// GATHER: forward (config C5 row pass) reads its row from the all-to-all receive blocks;
+// inverse (distributed inverse, F4) writes its natural-order row into the send blocks.
 struct GatherArgs {
-  const void* in;             // recv buffer (GATHER) or nullptr
-  uint32_t log_w;             // log2(N2/G): width of one received block
+  void* ext;                  // receive buffer (forward) / send buffer (inverse), or nullptr
+  uint32_t log_w;             // log2(N2/G): width of one block
   uint32_t log_rows_local;    // log2(N1/G): rows per block
 };
 
@@ -116,7 +118,15 @@ __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* 
 #pragma unroll
         for (int q = 0; q < G; ++q)
 #pragma unroll
-          for (int h = 0; h < S; ++h) xb[h * D + c[q]] = v[q * S + h];
+          for (int h = 0; h < S; ++h) {
+            const int i = h * D + c[q];
+            if constexpr (GATHER) {  // scatter: element i of row `row` -> block i >> log_w
+              const int hb = i >> ga.log_w, off = i & ((1 << ga.log_w) - 1);
+              reinterpret_cast<W*>(ga.ext)[(((size_t)hb << ga.log_rows_local) + row) << ga.log_w | off] = v[q * S + h];
+            } else {
+              xb[i] = v[q * S + h];
+            }
+          }
       }
     }
   } else {
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__(ContigShape<LOGN, LE>::THREADS, ContigShape<LO
     const bool active = b < batch;
     W* xb = x + b * Sh::N;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    contig_round<W, LOGN, LE, INV, GATHER, PLO1, r0>(v, xb, reinterpret_cast<const W*>(ga.in), b, ga, sm + slot * Sh::N,
+    contig_round<W, LOGN, LE, INV, GATHER, PLO1, r0>(v, xb, reinterpret_cast<const W*>(ga.ext), b, ga, sm + slot * Sh::N,
                                                      t, active, tw, m, norm != 0);
   }
 }
@@ -455,11 +465,97 @@ cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, vo
 
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
                                uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s) {
-  GatherArgs ga{recv, (uint32_t)logn2 - log_world, log_rows_local};
+  GatherArgs ga{const_cast<void*>(recv), (uint32_t)logn2 - log_world, log_rows_local};
   const size_t rows = (size_t)1 << log_rows_local;
   if (wbytes == 8)
     return contig_dispatch<uint64_t, false, true, 5, kContigMaxLog64>(logn2, out, rows, tw, p, true, ga, s);
   return contig_dispatch<uint32_t, false, true, 5, kContigMaxLog32>(logn2, out, rows, tw, p, true, ga, s);
+}
+
+cudaError_t launch_rows_scatter(int wbytes, int logn2, const void* in, void* send, uint32_t log_rows_local,
+                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s) {
+  GatherArgs ga{send, (uint32_t)logn2 - log_world, log_rows_local};
+  const size_t rows = (size_t)1 << log_rows_local;
+  void* x = const_cast<void*>(in);  // read only: the inverse's scatter writes to `send`
+  if (wbytes == 8)
+    return contig_dispatch<uint64_t, true, true, 5, kContigMaxLog64>(logn2, x, rows, tw_inv, p, true, ga, s);
+  return contig_dispatch<uint32_t, true, true, 5, kContigMaxLog32>(logn2, x, rows, tw_inv, p, true, ga, s);
+}
+
+// ----------------------------------------------------------------- block transpose
+// dst[j][i][k] = src[i][j][k] (i < n0, j < n1, k < n2): the pack / unpack of the
+// distributed four-step's contiguous-layout variants (F4).  HBM-bound copy; each warp
+// moves one contiguous run of n2 words with 16-byte accesses when aligned.
+template <class W>
+__global__ void k_block_transpose(W* __restrict__ dst, const W* __restrict__ src, uint64_t n0, uint64_t n1,
+                                  uint64_t n2) {
+  const uint64_t runs = n0 * n1;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int PER = 16 / sizeof(W);
+  const bool vec = (n2 % PER) == 0;
+  for (uint64_t rr = warp; rr < runs; rr += nwarps) {
+    const uint64_t i = rr / n1, j = rr % n1;
+    const W* s = src + rr * n2;
+    W* d = dst + (j * n0 + i) * n2;
+    if (vec) {
+      for (uint64_t k = (uint64_t)lane * PER; k < n2; k += 32 * PER)
+        *reinterpret_cast<uint4*>(d + k) = __ldcs(reinterpret_cast<const uint4*>(s + k));
+    } else {
+      for (uint64_t k = lane; k < n2; k += 32) d[k] = s[k];
+    }
+  }
+}
+
+cudaError_t launch_block_transpose(int wbytes, void* dst, const void* src, uint64_t n0, uint64_t n1, uint64_t n2,
+                                   cudaStream_t s) {
+  if (!n0 || !n1 || !n2) return cudaSuccess;
+  const int th = 256;
+  const uint64_t warps = n0 * n1;
+  uint64_t g = (warps * 32 + th - 1) / th;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  const unsigned grid = (unsigned)(g < cap ? g : cap);
+  if (wbytes == 8)
+    k_block_transpose<uint64_t><<<grid, th, 0, s>>>((uint64_t*)dst, (const uint64_t*)src, n0, n1, n2);
+  else
+    k_block_transpose<uint32_t><<<grid, th, 0, s>>>((uint32_t*)dst, (const uint32_t*)src, n0, n1, n2);
+  return cudaGetLastError();
+}
+
+unsigned elementwise_grid(size_t n, int threads);
+
+// ----------------------------------------------------------------- three-prime CRT (F3)
+// Garner's mixed-radix reconstruction of x in [0, p0 p1 p2) from residues r_i < p_i
+// (the RNS use of P:21): v0 = r0, v1 = (r1 - v0) p0^{-1} mod p1,
+// v2 = ((r2 - v0) p0^{-1} - v1) p1^{-1} mod p2, x = v0 + v1 p0 + v2 p0 p1.  Every
+// multiply by a constant is a Shoup multiply with a host-precomputed W';
+// the subtractions add a multiple of the modulus so each Shoup input stays < 2^32.
+__global__ void k_crt3(uint64_t* __restrict__ out, const uint32_t* __restrict__ r0, const uint32_t* __restrict__ r1,
+                       const uint32_t* __restrict__ r2, size_t n, Crt3Consts k) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t v0 = __ldcs(r0 + i);
+    uint32_t v1 = shoup_mul<uint32_t>(__ldcs(r1 + i) + k.K1 - v0, k.c01, k.c01p, k.p1);  // [0, 2 p1)
+    v1 = csub<uint32_t>(v1, k.p1);
+    uint32_t u = shoup_mul<uint32_t>(__ldcs(r2 + i) + k.K2 - v0, k.c02, k.c02p, k.p2);  // [0, 2 p2)
+    uint32_t v2 = shoup_mul<uint32_t>(u + k.K3 - v1, k.c12, k.c12p, k.p2);
+    v2 = csub<uint32_t>(v2, k.p2);
+    // x = v0 + v1 p0 + v2 (p0 p1): the last term is up to 2^92, so 128-bit
+    const uint64_t a = (uint64_t)v0 + (uint64_t)v1 * k.p0;  // < p0 p1 <= 2^62
+    const uint64_t lo = (uint64_t)v2 * k.p01, hi = __umul64hi((uint64_t)v2, k.p01);
+    const uint64_t xlo = lo + a;
+    const uint64_t xhi = hi + (xlo < lo ? 1u : 0u);
+    __stcs(reinterpret_cast<ulonglong2*>(out) + i, make_ulonglong2(xlo, xhi));
+  }
+}
+
+cudaError_t launch_crt3(uint64_t* out, const uint32_t* r0, const uint32_t* r1, const uint32_t* r2, size_t n,
+                        const Crt3Consts& k, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const int th = 256;
+  k_crt3<<<elementwise_grid(n, th), th, 0, s>>>(out, r0, r1, r2, n, k);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
@@ -471,7 +567,7 @@ cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsP
                  : cols_dispatch<uint32_t, false, kColsMinLog, kColsMaxLog32>(logn, x, prm, t, p, s);
 }
 
-static unsigned elementwise_grid(size_t n, int threads) {
+unsigned elementwise_grid(size_t n, int threads) {
   size_t g = (n + threads - 1) / threads;
   size_t cap = (size_t)num_sms() * 16;
   return (unsigned)(g < cap ? (g ? g : 1) : cap);

@@ -140,7 +140,8 @@ struct ntt_plan_s {
   std::vector<void*> owned;
   // lazily built tables for the distributed four-step entry points (guarded by mu)
   std::mutex mu;
-  std::map<unsigned, void*> extra_sub;  // log2 N -> omega_N^e table
+  std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e table
+  std::map<unsigned, void*> extra_sub_inv;  // log2 N -> omega_N^{-e} table
   // host-buffer executor (ntt_execute_host): pipeline streams and events
   static constexpr int kSlots = 3;
   cudaStream_t pipe[kSlots] = {nullptr, nullptr, nullptr};
@@ -217,16 +218,19 @@ std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
   }
 }
 
-// Table omega_N^e (e < N/2) for N = 2^logn, built once per plan (distributed entry points).
-ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out) {
+// Per-stage table of omega_N (inverse: omega_N^{-1}) for N = 2^logn, built once per plan
+// (distributed entry points).
+ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out, bool inverse = false) {
   std::lock_guard<std::mutex> lk(pl->mu);
-  auto it = pl->extra_sub.find(logn);
-  if (it != pl->extra_sub.end()) { *out = it->second; return NTT_OK; }
+  auto& cache = inverse ? pl->extra_sub_inv : pl->extra_sub;
+  auto it = cache.find(logn);
+  if (it != cache.end()) { *out = it->second; return NTT_OK; }
   const uint64_t L = (uint64_t)1 << pl->ell, Nn = (uint64_t)1 << logn;
   void* d = nullptr;
-  ntt_status st = upload(pl, make_stage_table(pl->p, powmod(pl->omega, L / Nn, pl->p), logn, pl->bits), &d);
+  const uint64_t root = powmod(inverse ? pl->omega_inv : pl->omega, L / Nn, pl->p);
+  ntt_status st = upload(pl, make_stage_table(pl->p, root, logn, pl->bits), &d);
   if (st != NTT_OK) return st;
-  pl->extra_sub[logn] = d;
+  cache[logn] = d;
   *out = d;
   return NTT_OK;
 }
@@ -591,8 +595,10 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, nt
   return st;
 }
 
-ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
-                             ntt_stream_t stream) {
+// Column half of the distributed four-step (forward: column NTTs then the twiddle;
+// inverse: the inverse twiddle then inverse column NTTs, passes in reverse order).
+static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
+                                     ntt_stream_t stream, bool inverse) {
   t_launches = 0;
   if (!pl || !x || !aligned16(x) || world == 0 || (world & (world - 1)) || rank >= world) return NTT_ERR_ARG;
   if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
@@ -614,13 +620,14 @@ ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned ran
     ntt_status st = ensure_fourstep_tables(pl);  // before reading pl->H
     if (st != NTT_OK) return st;
   }
-  cudaError_t e = cudaSuccess;
+  std::vector<nttb::ColsParams> prms(nc);
   unsigned outer = 0;
-  for (unsigned j = 0; j < nc && e == cudaSuccess; ++j) {
+  for (unsigned j = 0; j < nc; ++j) {
     const unsigned logN = cp[j];
     // local block = rows of this sub-level x local width
     const unsigned logS = (ell1 - outer - logN) + log_wl;
-    nttb::ColsParams prm{};
+    nttb::ColsParams& prm = prms[j];
+    prm = nttb::ColsParams{};
     prm.log_S = logS;
     prm.log_colgroups = logS - logC;
     prm.n_tiles = ((uint64_t)1 << outer) << prm.log_colgroups;
@@ -628,20 +635,34 @@ ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned ran
     prm.ell = pl->ell;
     prm.H = pl->H;
     prm.twiddle = 1;
-    prm.normalize = 0;
+    prm.normalize = (inverse && j == 0) ? 1 : 0;  // the inverse's last pass writes canonical values
     prm.shard = 1;
     prm.log_local_w = log_wl;
     prm.log_n2 = ell2;
     prm.col0 = rank << log_wl;
-    void* subf = nullptr;
-    ntt_status st = sub_table(pl, logN, &subf);
-    if (st != NTT_OK) return st;
-    nttb::DevTables t{subf, subf, pl->fa, pl->fb};
-    e = nttb::launch_cols(pl->wbytes, (int)logN, false, x, prm, t, pl->p, (cudaStream_t)stream);
-    ++t_launches;
     outer += logN;
   }
+  cudaError_t e = cudaSuccess;
+  for (unsigned jj = 0; jj < nc && e == cudaSuccess; ++jj) {
+    const unsigned j = inverse ? nc - 1 - jj : jj;
+    void* sub = nullptr;
+    ntt_status st = sub_table(pl, cp[j], &sub, inverse);
+    if (st != NTT_OK) return st;
+    nttb::DevTables t{sub, sub, pl->fa, pl->fb};
+    e = nttb::launch_cols(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
+    ++t_launches;
+  }
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
+                             ntt_stream_t stream) {
+  return fourstep_cols_impl(pl, ell1, x, rank, world, stream, false);
+}
+
+ntt_status ntt_fourstep_cols_inv(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
+                                 ntt_stream_t stream) {
+  return fourstep_cols_impl(pl, ell1, x, rank, world, stream, true);
 }
 
 ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,
@@ -666,6 +687,66 @@ ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, voi
                                            (cudaStream_t)stream);
   ++t_launches;
   (void)rank;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_fourstep_rows_inv(ntt_plan_t pl, unsigned ell1, const void* in, void* send, unsigned rank,
+                                 unsigned world, ntt_stream_t stream) {
+  t_launches = 0;
+  if (!pl || !in || !send || !aligned16(in) || in == send || world == 0 || (world & (world - 1)) || rank >= world)
+    return NTT_ERR_ARG;
+  if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
+  const unsigned ell2 = pl->ell - ell1;
+  const unsigned cmax = pl->wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
+  if (ell2 > cmax || ell2 < 5) return NTT_ERR_UNSUPPORTED;
+  unsigned lw = 0;
+  while ((1u << lw) < world) ++lw;
+  if (lw > ell1 || lw > ell2) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  void* subi = nullptr;
+  ntt_status st = sub_table(pl, ell2, &subi, true);
+  if (st != NTT_OK) return st;
+  cudaError_t e = nttb::launch_rows_scatter(pl->wbytes, (int)ell2, in, send, ell1 - lw, lw, subi, pl->p,
+                                            (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_block_transpose(void* dst, const void* src, size_t n0, size_t n1, size_t n2, unsigned word_bytes,
+                               ntt_stream_t stream) {
+  t_launches = 0;
+  if ((word_bytes != 4 && word_bytes != 8)) return NTT_ERR_ARG;
+  if (!n0 || !n1 || !n2) return NTT_OK;
+  if (!dst || !src || dst == src || !aligned16(dst) || !aligned16(src)) return NTT_ERR_ARG;
+  if (n0 > SIZE_MAX / n1 || n0 * n1 > SIZE_MAX / n2 || n0 * n1 * n2 > SIZE_MAX / word_bytes) return NTT_ERR_ARG;
+  cudaError_t e = nttb::launch_block_transpose((int)word_bytes, dst, src, n0, n1, n2, (cudaStream_t)stream);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_crt3(uint64_t* out, const uint32_t* r0, const uint32_t* r1, const uint32_t* r2, size_t n,
+                    uint32_t p0, uint32_t p1, uint32_t p2, ntt_stream_t stream) {
+  t_launches = 0;
+  const uint32_t ps[3] = {p0, p1, p2};
+  for (uint32_t q : ps)
+    if (q < 3 || !(q & 1) || q >= (1u << 30) || !is_prime_u64(q)) return NTT_ERR_MODULUS;
+  if (p0 == p1 || p0 == p2 || p1 == p2) return NTT_ERR_MODULUS;
+  if (!n) return NTT_OK;
+  if (!out || !r0 || !r1 || !r2 || !aligned16(out) || n > SIZE_MAX / 16) return NTT_ERR_ARG;
+  nttb::Crt3Consts k{};
+  k.p0 = p0; k.p1 = p1; k.p2 = p2;
+  auto shoup32 = [](uint64_t w, uint64_t p) { return (uint32_t)(((u128)w << 32) / p); };
+  k.c01 = (uint32_t)powmod(p0 % p1, p1 - 2, p1); k.c01p = shoup32(k.c01, p1);
+  k.c02 = (uint32_t)powmod(p0 % p2, p2 - 2, p2); k.c02p = shoup32(k.c02, p2);
+  k.c12 = (uint32_t)powmod(p1 % p2, p2 - 2, p2); k.c12p = shoup32(k.c12, p2);
+  // K_i = ceil(bound / p) * p >= the subtracted value's bound; every Shoup input
+  // (< K + p < 2^31 + 2^30) stays below beta = 2^32 (any T < beta)
+  k.K1 = (uint32_t)(((uint64_t)p0 + p1 - 1) / p1 * p1);
+  k.K2 = (uint32_t)(((uint64_t)p0 + p2 - 1) / p2 * p2);
+  k.K3 = (uint32_t)(((uint64_t)p1 + p2 - 1) / p2 * p2);
+  k.p01 = (uint64_t)p0 * p1;
+  cudaError_t e = nttb::launch_crt3(out, r0, r1, r2, n, k, (cudaStream_t)stream);
+  ++t_launches;
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 

@@ -12,6 +12,13 @@
       ntt_fourstep_rows  (row NTTs of length N2 over the G received blocks, normalised)
   and ends with flat positions [g L/G, (g+1) L/G) of Algorithm 1's bit-reversed output.
 
+The same split runs backwards (`FourStepInverse`): row inverse NTTs on the
+rank's rows of the bit-reversed spectrum, scattered straight into the all-to-all send blocks
+(`ntt_fourstep_rows_inv`), the all-to-all, then the inverse twiddle and column inverse NTTs
+(`ntt_fourstep_cols_inv`), leaving the natural-order column shard of L*a.  `FourStepForwardContig` /
+`FourStepInverseContig` take / return contiguous natural-order shards (rank g holds x[g L/G, (g+1) L/G))
+at the cost of a second all-to-all and one block transpose (`ntt_block_transpose`).
+
 The collective is `torch.distributed.all_to_all_single` on the NCCL process group (gloo in CPU tests);
 the compute steps are the CUDA kernels behind the C ABI (`Plan.fourstep_cols/rows`).  The layout
 helpers below are pure host logic, shared by the product path and the CPU tests.
@@ -116,4 +123,72 @@ class FourStepForward:
         self.cols(x_shard, stream)
         self.exchange(x_shard, recv)
         self.rows(recv, out, stream)
+        return out
+
+
+def _exchange(send, recv, world, group):
+    import torch.distributed as dist
+    if world == 1:
+        recv.copy_(send)
+    else:
+        dist.all_to_all_single(recv, send, group=group)
+
+
+class FourStepInverse:
+    """Distributed inverse of FourStepForward: `rows` (this rank's N1/G rows of the bit-reversed spectrum,
+    layout.shard_words words, left unmodified) -> `out` = natural-order column shard of L*a
+    (N1 x N2/G row-major).  send: scratch of shard_words words."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None):
+        self.plan, self.layout, self.rank, self.group = plan, layout, rank, group
+
+    def rows_inv(self, rows, send, stream=None):
+        self.plan.fourstep_rows_inv(self.layout.ell1, rows, send, self.rank, self.layout.world, stream=stream)
+
+    def exchange(self, send, out):
+        _exchange(send, out, self.layout.world, self.group)
+
+    def cols_inv(self, out, stream=None):
+        self.plan.fourstep_cols_inv(self.layout.ell1, out, self.rank, self.layout.world, stream=stream)
+
+    def __call__(self, rows, send, out, stream=None):
+        self.rows_inv(rows, send, stream)
+        self.exchange(send, out)
+        self.cols_inv(out, stream)
+        return out
+
+
+class FourStepForwardContig:
+    """Forward NTT of one transform from a contiguous natural-order shard (rank g holds x[g L/G, (g+1) L/G),
+    i.e. rows [g N1/G, (g+1) N1/G) of the N1 x N2 view) to the contiguous bit-reversed output shard:
+    block-transpose pack, all-to-all (-> column shard), FourStepForward.  x is clobbered; buf: scratch."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None):
+        self.fwd = FourStepForward(plan, layout, rank, group)
+        self.layout = layout
+
+    def __call__(self, x, buf, out, stream=None):
+        from . import block_transpose
+        lay = self.layout
+        # rows x (G blocks of local_width) -> G blocks of (rows x local_width)
+        block_transpose(buf, x, lay.rows_per_rank, lay.world, lay.local_width, stream=stream)
+        _exchange(buf, x, lay.world, self.fwd.group)          # x <- column shard
+        return self.fwd(x, buf, out, stream)
+
+
+class FourStepInverseContig:
+    """Inverse of FourStepForwardContig: contiguous bit-reversed shard in (unmodified) -> contiguous
+    natural-order shard of L*a in `out`.  send, buf: scratch."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None):
+        self.inv = FourStepInverse(plan, layout, rank, group)
+        self.layout = layout
+
+    def __call__(self, rows, send, buf, out, stream=None):
+        from . import block_transpose
+        lay = self.layout
+        self.inv(rows, send, buf, stream)                      # buf <- natural column shard (N1 x Wl)
+        _exchange(buf, send, lay.world, self.inv.group)        # block g = rows [rank R, ...) x cols of rank g
+        # G blocks of (rows x local_width) -> rows x (G blocks of local_width)
+        block_transpose(out, send, lay.world, lay.rows_per_rank, lay.local_width, stream=stream)
         return out

@@ -101,6 +101,65 @@ def test_fourstep_world2_gloo(tmp_path, ell, ell1):
         assert (np.load(tmp_path / f"cov{g}.npy") == 1).all()
 
 
+def _emulated_rows_inv(rows, layout, p, w):
+    """ntt_fourstep_rows_inv semantics: inverse NTT (root w^{-N1}, unscaled) of each of the rank's rows,
+    row r's column block h -> block h of the send buffer."""
+    import oracle
+    G, R, Wl, N2 = layout.world, layout.rows_per_rank, layout.local_width, layout.N2
+    nat = oracle.ntt_inverse(p, pow(w, layout.N1, p), rows.reshape(R, N2))  # R x N2 natural
+    return np.concatenate([nat[:, h * Wl:(h + 1) * Wl].reshape(-1) for h in range(G)])
+
+
+def _emulated_cols_inv(shard, layout, rank, p, w):
+    """ntt_fourstep_cols_inv semantics: (r, c) *= w^{-c rev(r)}, then inverse length-N1 NTTs down columns."""
+    import oracle
+    N1, Wl = layout.N1, layout.local_width
+    m = shard.reshape(N1, Wl).copy()
+    wi = pow(w, p - 2, p)
+    c0, _ = layout.columns(rank)
+    for cl in range(Wl):
+        col = [int(m[r, cl]) * pow(wi, (c0 + cl) * _bitrev(r, layout.ell1), p) % p for r in range(N1)]
+        m[:, cl] = oracle.ntt_inverse(p, pow(w, layout.N2, p), np.array(col, dtype=np.uint64))
+    return m.reshape(-1)
+
+
+def _worker_inv(rank, world, port, ell, ell1, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    from paper_1205_2926_b200.dist import FourStepInverse, FourStepLayout
+    layout = FourStepLayout(ell, ell1, world)
+    p = P62
+    w = pow(3, (p - 1) // layout.L, p)
+    x = synth.uniform_mod(synth.config_seed(5), 1, 0, layout.L, p)
+    spec = oracle.ntt_forward(p, w, x)
+    a, b = layout.output_range(rank)
+    send = _emulated_rows_inv(spec[a:b], layout, p, w)
+    st = torch.from_numpy(send.view(np.int64).copy())
+    recv = torch.empty_like(st)
+    FourStepInverse(plan=None, layout=layout, rank=rank).exchange(st, recv)  # the product's collective
+    out = _emulated_cols_inv(recv.numpy().view(np.uint64), layout, rank, p, w)
+    np.save(os.path.join(out_dir, f"inv{rank}.npy"), out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ell,ell1", [(10, 5), (9, 4)])
+def test_fourstep_inverse_world2_gloo(tmp_path, ell, ell1):
+    """F4 layout: rows_inv -> all_to_all_single (gloo) -> cols_inv returns the column shards of L*x."""
+    import synth
+    from paper_1205_2926_b200.dist import FourStepLayout, scatter_columns
+    world = 2
+    mp.spawn(_worker_inv, args=(world, _free_port(), ell, ell1, str(tmp_path)), nprocs=world, join=True)
+    layout = FourStepLayout(ell, ell1, world)
+    p = P62
+    x = synth.uniform_mod(synth.config_seed(5), 1, 0, layout.L, p)
+    Lx = np.array([(int(v) * layout.L) % p for v in x], dtype=np.uint64)
+    for g in range(world):
+        assert np.array_equal(np.load(tmp_path / f"inv{g}.npy"), scatter_columns(Lx, layout, g)), g
+
+
 def test_layout_helpers():
     from paper_1205_2926_b200.dist import FourStepLayout, batch_shard
     lay = FourStepLayout(28, 14, 8)

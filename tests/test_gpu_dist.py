@@ -49,3 +49,110 @@ def test_fourstep_virtual_ranks(ntt, p, bits, ell, ell1, G):
     got = torch.cat(outs)
     assert torch.equal(got.view(torch.int64 if bits == 64 else torch.int32),
                        ref.view(torch.int64 if bits == 64 else torch.int32))
+
+
+def _a2a(sends, G):
+    """all_to_all_single emulation: rank h receives chunk h of every rank g, in rank order."""
+    n = sends[0].numel() // G
+    return [torch.cat([sends[g][h * n:(h + 1) * n] for g in range(G)]) for h in range(G)]
+
+
+def _ieq(a, b, bits):
+    dt = torch.int64 if bits == 64 else torch.int32
+    return torch.equal(a.view(dt), b.view(dt))
+
+
+@pytest.mark.parametrize("p,bits,ell,ell1,G", [
+    (P62, 64, 12, 6, 2), (P62, 64, 16, 8, 4), (P30, 32, 16, 8, 2), (P62, 64, 20, 10, 8), (P62, 64, 28, 14, 8),
+])
+def test_fourstep_inverse_virtual_ranks(ntt, p, bits, ell, ell1, G):
+    """F4: distributed inverse (rows_inv -> all-to-all -> cols_inv) of the single-GPU forward output
+    gives the column shards of L*x, i.e. exactly ntt_inverse(ntt_forward(x)) resharded."""
+    from paper_1205_2926_b200.dist import FourStepLayout
+    import synth
+    lay = FourStepLayout(ell, ell1, G)
+    L, N1, N2, Wl = lay.L, lay.N1, lay.N2, lay.local_width
+    w = pow(3, (p - 1) // L, p)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(5), 1, bound=p)
+    spec = x.clone()
+    plan.forward(spec)
+    ref = spec.clone()
+    plan.inverse(ref)  # = L*x, natural order (itself pinned vs the oracle in test_gpu_parity)
+    rows = [spec[g * lay.shard_words:(g + 1) * lay.shard_words].clone() for g in range(G)]
+    del spec
+    sends = []
+    for g in range(G):
+        send = torch.empty(lay.shard_words, dtype=dt, device="cuda")
+        keep = rows[g].clone()
+        plan.fourstep_rows_inv(ell1, rows[g], send, g, G)
+        assert _ieq(rows[g], keep, bits), "rows_inv must not modify its input"
+        sends.append(send)
+    del rows
+    recvs = _a2a(sends, G)
+    del sends
+    for h in range(G):
+        plan.fourstep_cols_inv(ell1, recvs[h], h, G)
+        want = ref.view(N1, N2)[:, h * Wl:(h + 1) * Wl].contiguous().view(-1)
+        assert _ieq(recvs[h], want, bits), h
+
+
+@pytest.mark.parametrize("p,bits,ell,ell1,G", [(P62, 64, 16, 8, 4), (P30, 32, 16, 8, 2), (P62, 64, 24, 12, 8)])
+def test_fourstep_contig_roundtrip_virtual_ranks(ntt, p, bits, ell, ell1, G):
+    """F4: contiguous natural shards -> (pack, all-to-all, cols, all-to-all, rows) -> contiguous shards of
+    Alg. 1's output, bit-exact vs ntt_forward; then back with the contiguous inverse to L*x."""
+    from paper_1205_2926_b200.dist import FourStepLayout
+    import synth
+    lay = FourStepLayout(ell, ell1, G)
+    L, R, Wl, S = lay.L, lay.rows_per_rank, lay.local_width, lay.shard_words
+    w = pow(3, (p - 1) // L, p)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(5), 2, bound=p)
+    spec_ref = x.clone()
+    plan.forward(spec_ref)
+    # forward, contiguous input: pack each rank's rows into send blocks
+    bufs = [torch.empty(S, dtype=dt, device="cuda") for _ in range(G)]
+    for g in range(G):
+        ntt.block_transpose(bufs[g], x[g * S:(g + 1) * S], R, G, Wl)
+    cols = _a2a(bufs, G)
+    for g in range(G):
+        plan.fourstep_cols(ell1, cols[g], g, G)
+    recv = _a2a(cols, G)
+    outs = []
+    for g in range(G):
+        o = torch.empty(S, dtype=dt, device="cuda")
+        plan.fourstep_rows(ell1, recv[g], o, g, G)
+        outs.append(o)
+    assert _ieq(torch.cat(outs), spec_ref, bits)
+    # inverse, contiguous output
+    sends = []
+    for g in range(G):
+        s_ = torch.empty(S, dtype=dt, device="cuda")
+        plan.fourstep_rows_inv(ell1, outs[g], s_, g, G)
+        sends.append(s_)
+    colsh = _a2a(sends, G)
+    for g in range(G):
+        plan.fourstep_cols_inv(ell1, colsh[g], g, G)
+    back = _a2a(colsh, G)
+    res = []
+    for g in range(G):
+        o = torch.empty(S, dtype=dt, device="cuda")
+        ntt.block_transpose(o, back[g], G, R, Wl)
+        res.append(o)
+    got = torch.cat(res).cpu().numpy().astype(object)
+    want = (x.cpu().numpy().astype(object) * L) % p
+    assert (got == want).all()
+
+
+def test_block_transpose(ntt):
+    for dt, n0, n1, n2 in ((torch.uint64, 3, 5, 16), (torch.uint32, 4, 8, 32), (torch.uint64, 2, 3, 7),
+                           (torch.uint32, 1, 1, 1)):
+        src = torch.arange(n0 * n1 * n2, dtype=torch.int64, device="cuda").to(
+            torch.int64 if dt == torch.uint64 else torch.int32)
+        dst = torch.empty_like(src)
+        ntt.block_transpose(dst, src, n0, n1, n2)
+        assert torch.equal(dst.view(n1, n0, n2), src.view(n0, n1, n2).transpose(0, 1))

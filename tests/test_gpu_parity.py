@@ -307,3 +307,50 @@ def test_edge_cases(ntt):
     dx = to_dev(x, 64)
     plan.forward(dx)
     assert np.array_equal(to_host(dx), oracle.ntt_forward(p, root(p, 1 << ell), x))
+
+
+# ---- F3: three-prime CRT
+def test_crt3_parity(ntt):
+    """ntt_crt3 vs the oracle's textbook CRT on random residues (incl. p-1 and 0), bit-exact, ragged n."""
+    rng = np.random.default_rng(21)
+    for n in (1, 1000, 100003):
+        res = [rng.integers(0, q, n, dtype=np.uint64) for q in RNS]
+        for r in res:
+            r[0], r[-1] = 0, 0
+        res[0][n // 2] = RNS[0] - 1
+        res[2][n // 3] = RNS[2] - 1
+        d = [torch.from_numpy(r.astype(np.uint32)).cuda() for r in res]
+        out = torch.empty(2 * n, dtype=torch.uint64, device="cuda")
+        ntt.crt3(out, *d, RNS)
+        o = out.cpu().numpy().view(np.uint64).reshape(n, 2)
+        got = [int(lo) + (int(hi) << 64) for lo, hi in o]
+        idx = list(range(n)) if n <= 1000 else list(rng.integers(0, n, 2000)) + [0, n // 2, n // 3, n - 1]
+        want = oracle.crt([r[idx] for r in res], RNS)
+        assert [got[i] for i in idx] == want
+
+
+def test_config3_exact_integer_product(ntt):
+    """C3 + F3 end to end: three-prime cyclic convolutions of length 2^16 (2^15 coefficients < 2^20,
+    zero-padded) lifted by ntt_crt3 equal numpy's exact integer convolution, on sampled pairs."""
+    ell, npairs, half = 16, 16, 1 << 15
+    L = 1 << ell
+    ah = synth.uniform_bits(synth.config_seed(3), 0, 0, npairs * half, 20).reshape(npairs, half)
+    bh = synth.uniform_bits(synth.config_seed(3), 1, 0, npairs * half, 20).reshape(npairs, half)
+    a = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
+    b = torch.zeros(npairs, L, dtype=torch.uint32, device="cuda")
+    a[:, :half] = torch.from_numpy(ah.astype(np.uint32)).cuda()
+    b[:, :half] = torch.from_numpy(bh.astype(np.uint32)).cuda()
+    res = []
+    for p in RNS:
+        plan = ntt.Plan(p, root(p, L), ell, 32)
+        ca, cb = a.clone(), b.clone()
+        plan.cyclic_convolve(ca, cb)
+        res.append(ca.reshape(-1))
+    out = torch.empty(2 * npairs * L, dtype=torch.uint64, device="cuda")
+    ntt.crt3(out, *res, RNS)
+    o = out.cpu().numpy().view(np.uint64).reshape(npairs, L, 2)
+    assert (o[:, :, 1] == 0).all()  # every coefficient < 2^55 < 2^64
+    for i in (0, npairs - 1):
+        exact = np.convolve(ah[i].astype(np.int64), bh[i].astype(np.int64))
+        assert np.array_equal(o[i, :2 * half - 1, 0].astype(np.int64), exact)
+        assert (o[i, 2 * half - 1:, 0] == 0).all()

@@ -283,3 +283,39 @@ def test_theorem1_bound_shoup_any_T():
             Q = (Wp * T) >> bb
             r = W * T - Q * p
             assert ((r >= 0) & (r < 2 * p)).all()
+
+
+# ---- F3: three-prime CRT (the RNS use of P:21)
+RNS3 = (469762049, 167772161, 998244353)
+
+
+def test_crt_recovers_known_integers():
+    """Residues of known integers (taken with Python's %, not the oracle) lift back to the integers,
+    including the range ends 0 and p0 p1 p2 - 1."""
+    M = RNS3[0] * RNS3[1] * RNS3[2]
+    rng = np.random.default_rng(11)
+    xs = [0, 1, M - 1, M // 2, RNS3[0], RNS3[0] * RNS3[1]] + [int(v) for v in rng.integers(0, 2**62, 50)]
+    xs += [(int(a) << 40) + int(b) for a, b in zip(rng.integers(0, 2**40, 20), rng.integers(0, 2**40, 20))]
+    xs = [x % M for x in xs]
+    res = [np.array([x % q for x in xs], dtype=np.uint64) for q in RNS3]
+    assert oracle.crt(res, RNS3) == xs
+
+
+def test_crt_gives_exact_integer_product():
+    """Config C3 in miniature: the CRT of the three residue convolutions (oracle NTT route) is the exact
+    integer product computed by numpy's integer convolution (coefficients < 2^55 < p0 p1 p2)."""
+    ell, half = 8, 128
+    L = 1 << ell
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 2**20, half, dtype=np.uint64)
+    b = rng.integers(0, 2**20, half, dtype=np.uint64)
+    exact = np.convolve(a.astype(np.int64), b.astype(np.int64))  # 2*half - 1 < L coefficients
+    pa = np.zeros(L, dtype=np.uint64); pa[:half] = a
+    pb = np.zeros(L, dtype=np.uint64); pb[:half] = b
+    res = []
+    for q in RNS3:
+        w = pow(3, (q - 1) // L, q)
+        res.append(oracle.ntt_inverse(q, w, oracle.pointwise(q, oracle.ntt_forward(q, w, pa),
+                                                            oracle.ntt_forward(q, w, pb), scale_L=L)))
+    got = oracle.crt(res, RNS3)
+    assert got[:2 * half - 1] == [int(v) for v in exact] and got[2 * half - 1:] == [0] * (L - 2 * half + 1)
