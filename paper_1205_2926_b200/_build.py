@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libntt_b200.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["plan.cu", "ntt_kernels.cu", "ntt_contig_tma.cu", "ntt_split2.cu", "synth.cu"]
+SOURCES = ["plan.cu", "ntt_kernels.cu", "ntt_contig_tma.cu", "ntt_cols_tma.cu", "ntt_split2.cu", "synth.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -1,0 +1,35 @@
+// fourstep.cuh -- the four-step twiddle of a column pass and the
+// global-column mapping of a distributed shard, shared by k_cols and k_cols_tma.
+#pragma once
+#include <cstdint>
+
+#include "internal.h"
+#include "modarith.cuh"
+#include "rounds.cuh"
+
+namespace nttb {
+
+// omega_L^e by the direct table (H == 0) or the factored tables
+// omega^{(e >> H) << H} * omega^{e & (2^H - 1)} (two Shoup multiplies).
+template <class W, bool PLO1>
+__device__ __forceinline__ W fourstep_twiddle(W val, uint32_t e, const ColsParams& prm, const TwPair<W>* __restrict__ fa,
+                                              const TwPair<W>* __restrict__ fb, const Mod<W>& m) {
+  W w, wp;
+  if (prm.H == 0) {
+    ldtw<W>(fa, e, w, wp);
+    return shoup_mul<W, PLO1>(val, w, wp, m);
+  }
+  ldtw<W>(fb, e & ((1u << prm.H) - 1), w, wp);
+  val = shoup_mul<W, PLO1>(val, w, wp, m);
+  ldtw<W>(fa, e >> prm.H, w, wp);
+  return shoup_mul<W, PLO1>(val, w, wp, m);
+}
+
+// Global column of local column `cloc` (ColsParams.shard: config C5 column shard).
+__device__ __forceinline__ uint32_t cols_global_column(uint32_t cloc, const ColsParams& prm) {
+  if (!prm.shard) return cloc;
+  const uint32_t rb = cloc >> prm.log_local_w, cl = cloc & ((1u << prm.log_local_w) - 1);
+  return (rb << prm.log_n2) | (prm.col0 + cl);
+}
+
+}  // namespace nttb

@@ -14,6 +14,7 @@ constexpr int kContigMaxLog32 = 15;  // 2^15 u32 = 128 KiB smem, 1024 threads x 
 constexpr int kColsMaxLog64 = 9;     // 2^9 rows x 16 u64 columns = 64 KiB tile
 constexpr int kColsMaxLog32 = 10;    // 2^10 rows x 32 u32 columns = 128 KiB tile
 constexpr int kColsMinLog = 4;
+constexpr int kColsTmaMaxLog = 9;    // TMA-staged column pass: N x 128-byte tiles <= 64 KiB, double-buffered
 // TMA-staged single-pass kernel (ntt_contig_tma.cu): double-buffered tiles of <= 64 KiB
 constexpr int kTmaMinLog = 8;
 constexpr int kTmaMaxLog64 = 13;
@@ -61,6 +62,10 @@ cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t ba
                           const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s);
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
                         uint64_t p, cudaStream_t s);
+// the same pass with TMA-staged, double-buffered tiles (ntt_cols_tma.cu)
+bool cols_tma_supported(int wbytes, int logn, const ColsParams& prm, const void* x);
+cudaError_t launch_cols_tma(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
+                            uint64_t p, cudaStream_t s);
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
                                uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s);
 // distributed inverse (F4): inverse row NTTs, natural-order rows scattered into the send blocks

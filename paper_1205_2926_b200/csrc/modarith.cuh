@@ -13,7 +13,27 @@ template <> struct alignas(8) TwPair<uint32_t> { uint32_t w, wp; };
 template <> struct alignas(16) TwPair<uint64_t> { uint64_t w, wp; };
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+#if defined(NTT_MULHI_CHAIN)
+// hi64(a b) as a 32-bit multiply-add carry chain (mad.lo.cc / madc.hi)
+__device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 a0,a1,b0,b1,t,m1,h0,h1;\n\t"
+      "mov.b64 {a0,a1}, %1;\n\tmov.b64 {b0,b1}, %2;\n\t"
+      "mul.hi.u32 t, a0, b0;\n\t"
+      "mad.lo.cc.u32 t, a0, b1, t;\n\t"
+      "madc.hi.u32 m1, a0, b1, 0;\n\t"
+      "mad.lo.cc.u32 t, a1, b0, t;\n\t"
+      "madc.hi.cc.u32 m1, a1, b0, m1;\n\t"
+      "addc.u32 h1, 0, 0;\n\t"
+      "mad.lo.cc.u32 h0, a1, b1, m1;\n\t"
+      "madc.hi.u32 h1, a1, b1, h1;\n\t"
+      "mov.b64 %0, {h0,h1};\n\t}"
+      : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+#else
 __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+#endif
 
 // Conditional subtraction x >= m ? x - m : x for x < 2m, m <= beta/2 (every use: m in
 // {p, 2p}, p < beta/4).  Then x - m lies in (-beta/2, beta/2), so its sign decides:

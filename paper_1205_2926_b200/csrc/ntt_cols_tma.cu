@@ -1,0 +1,242 @@
+// ntt_cols_tma.cu -- the four-step column pass with TMA staging.
+//
+// Same work as k_cols (ntt_kernels.cu): a tile is N rows x one 128-byte row segment
+// (C = 128 / sizeof(W) columns) of a block of the nested four-step view; the pass
+// runs length-N NTTs (Algorithm 1, Algorithm 3 / 4 butterflies) down the
+// C columns and applies the four-step twiddle omega^{c rev(r)} (forward: after,
+// inverse: omega^{-c rev(r)} before).  Here the tile comes in through one 3-D TMA
+// load (cp.async.bulk.tensor.3d, SWIZZLE_128B: 16-byte chunk ^= row mod 8) into one
+// of two shared-memory buffers while the CTA computes the other, and leaves through
+// a TMA bulk tensor store, so HBM latency is off the critical path of the strided
+// (2^9-2^19-word stride) column accesses.  Every round of a warp touches whole
+// 128-byte smem rows, so the swizzled layout is bank-conflict free.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+#include "fourstep.cuh"
+#include "internal.h"
+#include "modarith.cuh"
+#include "rounds.cuh"
+#include "tma.cuh"
+
+namespace nttb {
+
+template <class W, int LOGN, int LE> struct ColsTmaShape {
+  static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E, C = 128 / (int)sizeof(W), THREADS = T * C;
+  static constexpr int TILE_BYTES = N * 128;
+  static constexpr int BOX_ROWS = N < 256 ? N : 256;
+  static constexpr int BOXES = N / BOX_ROWS;
+  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + 1024;
+  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
+  using RC = Rounds<LOGN, LE>;
+  static constexpr int R = RC::R;
+  static_assert(TILE_BYTES % 1024 == 0, "tiles must keep the 1024-byte swizzle period");
+};
+
+template <class W, int LOGN, int LE>
+__device__ __forceinline__ void cols_tma_issue(const CUtensorMap* map, uint64_t tile, uint32_t log_colgroups,
+                                               uint32_t buf, uint32_t bar) {
+  using Sh = ColsTmaShape<W, LOGN, LE>;
+  const int bq = (int)(tile >> log_colgroups);
+  const int c0 = (int)(tile & ((1ull << log_colgroups) - 1)) * Sh::C;
+  mbar_expect_tx(bar, Sh::TILE_BYTES);
+#pragma unroll
+  for (int bx = 0; bx < Sh::BOXES; ++bx) tma_load_3d(buf + bx * Sh::BOX_ROWS * 128, map, c0, bx * Sh::BOX_ROWS, bq, bar);
+}
+
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
+__device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint32_t cglob, const ColsParams& prm,
+                                               const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
+                                               const TwPair<W>* __restrict__ fb, const Mod<W>& m,
+                                               const CUtensorMap* map, uint64_t next_tile, uint32_t next_buf,
+                                               uint32_t next_bar, bool prefetch) {
+  using Sh = ColsTmaShape<W, LOGN, LE>;
+  using RC = typename Sh::RC;
+  constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
+  constexpr int S = 1 << SR, G = Sh::E >> SR;
+  constexpr int D = Sh::N >> (LEVEL + SR), B = Sh::N >> LEVEL;
+  constexpr int C = Sh::C;
+  int c[G], blk[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = t + Sh::T * q;
+    blk[q] = g / D;
+    c[q] = g % D;
+  }
+  constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
+  constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
+#pragma unroll
+  for (int q = 0; q < G; ++q)
+#pragma unroll
+    for (int h = 0; h < S; ++h) {
+      const int row = blk[q] * B + h * D + c[q];
+      W val = sm[tswz<W>(row * C + cc)];
+      if constexpr (INV && first) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
+        if (prm.twiddle) {
+          const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+          const uint32_t e = (cglob * rv) << prm.log_tw_mul;
+          const uint32_t einv = (uint32_t)((((uint64_t)1 << prm.ell) - e) & (((uint64_t)1 << prm.ell) - 1));
+          val = fourstep_twiddle<W, PLO1>(val, einv, prm, fa, fb, m);
+        }
+      }
+      v[q * S + h] = val;
+    }
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  if constexpr (!last) {
+    __syncthreads();
+    if (prefetch && threadIdx.x == 0) {  // the other buffer's store has been issued: reuse it once read
+      bulk_wait_read0();
+      cols_tma_issue<W, LOGN, LE>(map, next_tile, prm.log_colgroups, next_buf, next_bar);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q)
+#pragma unroll
+    for (int h = 0; h < S; ++h) {
+      const int row = blk[q] * B + h * D + c[q];
+      W val = v[q * S + h];
+      if constexpr (last) {
+        if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
+          if (prm.twiddle) {
+            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+            val = fourstep_twiddle<W, PLO1>(val, (cglob * rv) << prm.log_tw_mul, prm, fa, fb, m);
+          }
+          if (prm.normalize) val = norm2<W>(val, m.p);
+        } else {
+          if (prm.normalize) val = norm4<W>(val, m.p, m.p2);
+        }
+      }
+      sm[tswz<W>(row * C + cc)] = val;  // each thread rewrites exactly the positions it read
+    }
+  if constexpr (!last) {
+    __syncthreads();
+    constexpr int nr = INV ? r - 1 : r + 1;
+    cols_tma_round<W, LOGN, LE, INV, PLO1, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, map, next_tile, next_buf,
+                                               next_bar, false);
+  }
+}
+
+template <class W, int LOGN, int LE, bool INV, bool PLO1>
+__global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaShape<W, LOGN, LE>::MINB)
+    k_cols_tma(const __grid_constant__ CUtensorMap tmap, ColsParams prm, const TwPair<W>* __restrict__ tw,
+               const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p) {
+  using Sh = ColsTmaShape<W, LOGN, LE>;
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t s0 = smem_u32(smem_raw);
+  unsigned char* base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * (size_t)Sh::TILE_BYTES);
+  const uint32_t buf_a[2] = {smem_u32(base), smem_u32(base + Sh::TILE_BYTES)};
+  const uint32_t bar_a[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
+  const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
+  const Mod<W> m = make_mod<W>(p);
+  const uint64_t cg_mask = (1ull << prm.log_colgroups) - 1;
+  if (threadIdx.x == 0) {
+    mbar_init(bar_a[0], 1);
+    mbar_init(bar_a[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint64_t tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE>(&tmap, tile, prm.log_colgroups, buf_a[0], bar_a[0]);
+  W v[Sh::E];
+  for (uint32_t it = 0; tile < prm.n_tiles; ++it, tile += gridDim.x) {
+    const int cur = it & 1;
+    const uint64_t next = tile + gridDim.x;
+    if constexpr (Sh::R == 1) {  // no exchange to hide the prefetch behind: issue it now
+      if (threadIdx.x == 0 && next < prm.n_tiles) {
+        bulk_wait_read0();
+        cols_tma_issue<W, LOGN, LE>(&tmap, next, prm.log_colgroups, buf_a[cur ^ 1], bar_a[cur ^ 1]);
+      }
+    }
+    mbar_wait(bar_a[cur], (it >> 1) & 1);
+    const uint32_t cglob = cols_global_column((uint32_t)((tile & cg_mask) * Sh::C + cc), prm);
+    W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
+    constexpr int r0 = INV ? Sh::R - 1 : 0;
+    cols_tma_round<W, LOGN, LE, INV, PLO1, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_a[cur ^ 1],
+                                               bar_a[cur ^ 1], Sh::R > 1 && next < prm.n_tiles);
+    fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int bq = (int)(tile >> prm.log_colgroups), c0 = (int)(tile & cg_mask) * Sh::C;
+#pragma unroll
+      for (int bx = 0; bx < Sh::BOXES; ++bx)
+        tma_store_3d(&tmap, c0, bx * Sh::BOX_ROWS, bq, buf_a[cur] + bx * Sh::BOX_ROWS * 128);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();  // smem must outlive the last bulk store
+}
+
+// ----------------------------------------------------------------- host side
+template <class W, int LOGN> struct ColsTmaLE {
+  static constexpr int value = sizeof(W) == 8 ? (LOGN < 4 ? LOGN : 4) : (LOGN < 5 ? LOGN : 5);
+};
+
+template <class W, int LOGN, bool INV, bool PLO1>
+static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
+  constexpr int LE = ColsTmaLE<W, LOGN>::value;
+  using Sh = ColsTmaShape<W, LOGN, LE>;
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const uint64_t S = 1ull << prm.log_S, blocks = prm.n_tiles >> prm.log_colgroups;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)S, (cuuint64_t)Sh::N, (cuuint64_t)blocks};
+  cuuint64_t strides[2] = {(cuuint64_t)(S * sizeof(W)), (cuuint64_t)(S * Sh::N * sizeof(W))};
+  cuuint32_t box[3] = {(cuuint32_t)Sh::C, (cuuint32_t)Sh::BOX_ROWS, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, x, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1>;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Sh::THREADS, Sh::SMEM);
+    if (occ <= 0) occ = 1;
+  }
+  const uint64_t maxg = (uint64_t)occ * sm_count();
+  const unsigned grid = (unsigned)(prm.n_tiles < maxg ? prm.n_tiles : maxg);
+  if (!grid) return cudaSuccess;
+  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(map, prm, reinterpret_cast<const TwPair<W>*>(INV ? tb.sub_inv : tb.sub_fwd),
+                                           reinterpret_cast<const TwPair<W>*>(tb.fa),
+                                           reinterpret_cast<const TwPair<W>*>(tb.fb), (W)p);
+  return cudaGetLastError();
+}
+
+template <class W, bool INV, int LO, int HI>
+static cudaError_t cols_tma_dispatch(int logn, void* x, const ColsParams& prm, const DevTables& tb, uint64_t p,
+                                     cudaStream_t s) {
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (logn == LO) {
+      if constexpr (sizeof(W) == 8) {
+        if ((p & 0xffffffffull) == 1) return run_cols_tma<W, LO, INV, true>(x, prm, tb, p, s);
+      }
+      return run_cols_tma<W, LO, INV, false>(x, prm, tb, p, s);
+    }
+    return cols_tma_dispatch<W, INV, LO + 1, HI>(logn, x, prm, tb, p, s);
+  }
+}
+
+bool cols_tma_supported(int wbytes, int logn, const ColsParams& prm, const void* x) {
+  // tiles of <= 64 KiB (two buffers per CTA); TMA needs a 16-byte aligned base and row stride
+  return logn >= kColsMinLog && logn <= kColsTmaMaxLog && ((uintptr_t)x & 15) == 0 &&
+         (((uint64_t)wbytes << prm.log_S) % 16) == 0 && (prm.n_tiles >> prm.log_colgroups) < (1ull << 31);
+}
+
+cudaError_t launch_cols_tma(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
+                            uint64_t p, cudaStream_t s) {
+  if (wbytes == 8)
+    return inverse ? cols_tma_dispatch<uint64_t, true, kColsMinLog, kColsTmaMaxLog>(logn, x, prm, t, p, s)
+                   : cols_tma_dispatch<uint64_t, false, kColsMinLog, kColsTmaMaxLog>(logn, x, prm, t, p, s);
+  return inverse ? cols_tma_dispatch<uint32_t, true, kColsMinLog, kColsTmaMaxLog>(logn, x, prm, t, p, s)
+                 : cols_tma_dispatch<uint32_t, false, kColsMinLog, kColsTmaMaxLog>(logn, x, prm, t, p, s);
+}
+
+}  // namespace nttb

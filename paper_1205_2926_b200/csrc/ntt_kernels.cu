@@ -14,6 +14,7 @@
 #include "internal.h"
 #include "modarith.cuh"
 #include "rounds.cuh"
+#include "fourstep.cuh"
 
 namespace nttb {
 
@@ -172,20 +173,6 @@ template <class W, int LOGN, int LE> struct ColsShape {
   using RC = Rounds<LOGN, LE>;
   static constexpr int R = RC::R;
 };
-
-template <class W, bool PLO1>
-__device__ __forceinline__ W fourstep_twiddle(W val, uint32_t e, const ColsParams& prm, const TwPair<W>* __restrict__ fa,
-                                              const TwPair<W>* __restrict__ fb, const Mod<W>& m) {
-  W w, wp;
-  if (prm.H == 0) {
-    ldtw<W>(fa, e, w, wp);
-    return shoup_mul<W, PLO1>(val, w, wp, m);
-  }
-  ldtw<W>(fb, e & ((1u << prm.H) - 1), w, wp);
-  val = shoup_mul<W, PLO1>(val, w, wp, m);
-  ldtw<W>(fa, e >> prm.H, w, wp);
-  return shoup_mul<W, PLO1>(val, w, wp, m);
-}
 
 template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
 __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int t, int cc, uint32_t cglob,

@@ -421,6 +421,15 @@ static cudaError_t launch_contig_any(int wbytes, int logn, bool inverse, bool no
   return nttb::launch_contig(wbytes, logn, inverse, normalize, x, batch, tw, p, s);
 }
 
+// Four-step column pass: the TMA-staged kernel where it applies (NTT_DISABLE_TMA=1
+// forces the register-direct one).
+static cudaError_t launch_cols_any(int wbytes, int logn, bool inverse, void* x, const nttb::ColsParams& prm,
+                                   const nttb::DevTables& t, uint64_t p, cudaStream_t s) {
+  if (tma_enabled() && nttb::cols_tma_supported(wbytes, logn, prm, x))
+    return nttb::launch_cols_tma(wbytes, logn, inverse, x, prm, t, p, s);
+  return nttb::launch_cols(wbytes, logn, inverse, x, prm, t, p, s);
+}
+
 static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
   t_launches = 0;
   if (!pl || (!x && batch) || (x && !aligned16(x))) return NTT_ERR_ARG;
@@ -470,7 +479,7 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
   if (!inverse) {
     for (unsigned j = 0; j + 1 < np && e == cudaSuccess; ++j) {
       nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
-      e = nttb::launch_cols(pl->wbytes, (int)pl->passes[j], false, x, cols_params(j, false), t, pl->p, s);
+      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], false, x, cols_params(j, false), t, pl->p, s);
       ++t_launches;
     }
     if (e == cudaSuccess) {
@@ -484,7 +493,7 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     ++t_launches;
     for (int j = (int)np - 2; j >= 0 && e == cudaSuccess; --j) {
       nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
-      e = nttb::launch_cols(pl->wbytes, (int)pl->passes[j], true, x, cols_params((unsigned)j, j == 0), t, pl->p, s);
+      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], true, x, cols_params((unsigned)j, j == 0), t, pl->p, s);
       ++t_launches;
     }
   }
@@ -649,7 +658,7 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
     ntt_status st = sub_table(pl, cp[j], &sub, inverse);
     if (st != NTT_OK) return st;
     nttb::DevTables t{sub, sub, pl->fa, pl->fb};
-    e = nttb::launch_cols(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
+    e = launch_cols_any(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
     ++t_launches;
   }
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);

@@ -19,7 +19,12 @@ from bench import CONFIGS, butterflies, root  # noqa: E402
 def main():
     key = sys.argv[1] if len(sys.argv) > 1 else "c2"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 20
-    cfg = dict(CONFIGS[key], key=key)
+    if key.startswith("x:"):  # x:p:bits:ell:batch[:ops]  custom shape, e.g. x:998244353:32:14:4096:fwd
+        f = key.split(":")
+        cfg = dict(primes=(int(f[1]),), bits=int(f[2]), ell=int(f[3]), batch=int(f[4]),
+                   ops=tuple((f[5] if len(f) > 5 else "fwd,inv").split(",")), key=key)
+    else:
+        cfg = dict(CONFIGS[key], key=key)
     L = 1 << cfg["ell"]
     dt = torch.uint64 if cfg["bits"] == 64 else torch.uint32
     plans = [ntt.Plan(p, root(p, L), cfg["ell"], cfg["bits"]) for p in cfg["primes"]]
