@@ -29,7 +29,7 @@ template <class W, int LOGN, int LE> struct ColsTmaShape {
   static constexpr int TILE_BYTES = N * 128;
   static constexpr int BOX_ROWS = N < 256 ? N : 256;
   static constexpr int BOXES = N / BOX_ROWS;
-  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + 1024;
+  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + NTT_SMEM_ALIGN_SLACK;
   static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;
   using RC = Rounds<LOGN, LE>;
   static constexpr int R = RC::R;

@@ -41,7 +41,7 @@ template <class W, int LOGN, int LE> struct TmaShape {
   static constexpr int BOX_ROWS = TILE_ROWS < 256 ? TILE_ROWS : 256;
   static constexpr int BOXES = TILE_ROWS / BOX_ROWS;
   static constexpr int BOX_BYTES = BOX_ROWS * 128;
-  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + 1024;
+  static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + 64 + NTT_SMEM_ALIGN_SLACK;
   using RC = Rounds<LOGN, LE>;
   static constexpr int R = RC::R;
   static_assert(R >= 2, "TMA kernel needs at least one exchange");

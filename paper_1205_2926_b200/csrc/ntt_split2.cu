@@ -17,6 +17,11 @@
 // distributed shared memory; CTA r finishes j in [rQ/K, (r+1)Q/K).  With PW the
 // pointwise product c = a b L^{-1} is formed while loading, so a cyclic
 // convolution needs no separate pointwise pass.
+//
+// Staging (inverse): each CTA's own block of the next transform (x, or a when PW) is
+// brought into shared memory by TMA (2-D tensor map of 128-byte rows, SWIZZLE_128B) once
+// the cluster's DSMEM epilogue no longer reads the buffer; the first round then reads it
+// from shared memory and only b (PW) comes from global memory.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -26,6 +31,7 @@
 #include "internal.h"
 #include "modarith.cuh"
 #include "rounds.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -46,16 +52,61 @@ template <int LOGQ, int LE, int K, int WB = 8> struct SplitShape {
   static constexpr int R = RC::R;
 };
 
+// Cluster barrier for write-after-read hazards only: every value the caller loaded before it
+// has already been consumed (in-order issue), so a relaxed arrive suffices and the
+// MEMBAR.ALL.GPU that cluster.sync() emits for its release is skipped.
+__device__ __forceinline__ void cluster_sync_war() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 struct PwArgs {
   const void* a;
   const void* b;
   uint64_t J, K, Kp;  // REDC constant and the Shoup constant restoring scale (beta L^{-1} mod p)
 };
 
+// Shared-memory staging of a transform (inverse only): this CTA's block of Q words, the
+// mbarrier right after it.  The forward reads both blocks straight from global memory in its
+// first round: measured faster than staging its own block (u32 2^16: 0.318 vs 0.320 ms,
+// u64 2^15: 0.203 vs 0.216 ms), since the other block's loads expose the same latency.
+template <class W, int LOGQ, int LE, int K, bool INV> struct SplitStaging {
+  static constexpr bool ON = INV;
+  static constexpr int Q = 1 << LOGQ;
+  static constexpr int WORDS = Q;
+};
+
+template <class W, int LOGQ, int LE, int K, bool INV>
+__device__ __forceinline__ uint32_t split_bar(const W* sm) {
+  return smem_u32(sm) + (uint32_t)(SplitStaging<W, LOGQ, LE, K, INV>::WORDS * sizeof(W));
+}
+
+// TMA loads of the staging of transform b (Q*sizeof(W)/128 rows of 128 bytes per block).
+template <class W, int LOGQ, int LE, int K, bool INV>
+__device__ __forceinline__ void split_issue_own(const CUtensorMap* map, size_t b, int rank, uint32_t dst, uint32_t bar) {
+  using St = SplitStaging<W, LOGQ, LE, K, INV>;
+  constexpr int ROWS = St::Q * (int)sizeof(W) / 128, BOX = ROWS < 256 ? ROWS : 256;
+  const int row0 = (int)((b * K + (size_t)rank) * (size_t)ROWS);
+  mbar_expect_tx(bar, (uint32_t)(St::WORDS * sizeof(W)));
+#pragma unroll
+  for (int bx = 0; bx < ROWS / BOX; ++bx) tma_load_2d(dst + bx * BOX * 128, map, 0, row0 + bx * BOX, bar);
+}
+
+// Staging state of the current transform: the 2-D map (128-byte rows) over x (forward,
+// plain inverse) or a (PW), the mbarrier parity to wait for, and the cluster's next
+// transform (next_b >= batch: none).  The tile sits at the start of shared memory and its
+// mbarrier right after it (k_splitk).
+struct SplitStage {
+  const CUtensorMap* map;
+  uint32_t phase;
+  size_t next_b, batch;
+};
+
+
 template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW, int r>
 __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int t, int rank,
                                             const TwPair<W>* __restrict__ tw_full, const Mod<W>& m,
-                                            const PwArgs& pw, size_t boff, cg::cluster_group& cluster) {
+                                            const PwArgs& pw, size_t boff, cg::cluster_group& cluster,
+                                            const SplitStage& st) {
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   using RC = typename Sh::RC;
   constexpr int Q = Sh::Q, SS = Sh::S_SPLIT, LOGL = Sh::LOGL;
@@ -73,6 +124,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
   constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
   if constexpr (first) {
+    // inverse: this CTA's block of the transform has been staged in shared memory
+    if constexpr (INV) mbar_wait(split_bar<W, LOGQ, LE, K, INV>(sm), st.phase);
     if constexpr (!INV) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
@@ -102,23 +155,32 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           }
           v[q * S + h] = u[0];
         }
-      cluster.sync();  // every CTA has read x_b: in-place stores below are safe
+      // every CTA has read x_b: in-place stores below are safe.  (Measured: the relaxed
+      // cluster_sync_war() here makes the forward 15-35% slower, so the full barrier stays.)
+      cluster.sync();
     } else {
-      // this CTA's block of the bit-reversed input (contiguous runs); PW: c = a b L^{-1}
+      // this CTA's block of the bit-reversed input (contiguous runs, from shared memory);
+      // PW: c = a b L^{-1} with b read from global memory 16 bytes at a time
+      constexpr int PER = 16 / (int)sizeof(W);
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const size_t off = (size_t)rank * Q + blk[q] * S;
-        if constexpr (PW) {
-          W av[S], bv[S];
-          load_run<W, S>(reinterpret_cast<const W*>(pw.a) + boff + off, av);
-          load_run<W, S>(reinterpret_cast<const W*>(pw.b) + boff + off, bv);
 #pragma unroll
-          for (int h = 0; h < S; ++h) {
-            W prod = mont_redc_mul<W>(av[h], bv[h], (W)pw.J, m.p);
-            v[q * S + h] = shoup_mul<W>(prod, (W)pw.K, (W)pw.Kp, m.p);
+        for (int h = 0; h < S; h += PER) {
+          W av[PER];
+          unpack16<W>(lds128(sm + tswz<W>(blk[q] * S + h)), av);
+          if constexpr (PW) {
+            W bv[PER];
+            const size_t off = (size_t)rank * Q + blk[q] * S + h;
+            unpack16<W>(__ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const W*>(pw.b) + boff + off)), bv);
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+              W prod = mont_redc_mul<W>(av[e], bv[e], (W)pw.J, m.p);
+              v[q * S + h + e] = shoup_mul<W>(prod, (W)pw.K, (W)pw.Kp, m.p);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < PER; ++e) v[q * S + h + e] = av[e];
           }
-        } else {
-          load_run<W, S>(xb + off, v + q * S);
         }
       }
       // no barrier needed here: the cross-CTA stores of the epilogue follow the
@@ -172,7 +234,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
         for (int tt = 0; tt < K; ++tt) xb[j + tt * Q] = norm4<W>(u[tt], m.p, m.p2);
       }
-      cluster.sync();  // the other CTAs are done reading this CTA's shared memory
+      cluster_sync_war();  // the other CTAs are done reading this CTA's shared memory
     }
   } else {
     __syncthreads();
@@ -182,27 +244,55 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       for (int h = 0; h < S; ++h) sm[sswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    split_round<W, LOGQ, LE, K, INV, PLO1, PW, nr>(v, xb, sm, t, rank, tw_full, m, pw, boff, cluster);
+    split_round<W, LOGQ, LE, K, INV, PLO1, PW, nr>(v, xb, sm, t, rank, tw_full, m, pw, boff, cluster, st);
   }
 }
 
 template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW>
 __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
                                   SplitShape<LOGQ, LE, K, (int)sizeof(W)>::MINB)
-    k_splitk(W* __restrict__ x, size_t batch, const TwPair<W>* __restrict__ tw_full, W p, PwArgs pw) {
+    k_splitk(const __grid_constant__ CUtensorMap tmap, W* __restrict__ x, size_t batch,
+             const TwPair<W>* __restrict__ tw_full, W p, PwArgs pw) {
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  W* sm = reinterpret_cast<W*>(smem_raw);
+  // staged (inverse): 1024-byte alignment for the TMA swizzle period (same offset in every
+  // CTA of the cluster); the forward keeps the plain Q-word buffer (measured: its extra
+  // 1 KiB of shared memory costs the forward 15%, through the L1 carveout)
+  unsigned char* base = smem_raw;
+  if constexpr (SplitStaging<W, LOGQ, LE, K, INV>::ON) {
+    const uint32_t s0 = smem_u32(smem_raw);
+    base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
+  }
+  W* sm = reinterpret_cast<W*>(base);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int t = threadIdx.x;
   const Mod<W> m = make_mod<W>(p);
+  SplitStage st{&tmap, 0u, 0, batch};
+  if constexpr (SplitStaging<W, LOGQ, LE, K, INV>::ON) {
+    if (threadIdx.x == 0) {
+      mbar_init(split_bar<W, LOGQ, LE, K, INV>(sm), 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   W v[Sh::E];
   const size_t groups = gridDim.x / K;
-  for (size_t b = blockIdx.x / K; b < batch; b += groups) {
+  size_t b = blockIdx.x / K;
+  if (SplitStaging<W, LOGQ, LE, K, INV>::ON && threadIdx.x == 0 && b < batch) split_issue_own<W, LOGQ, LE, K, INV>(st.map, b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
+  for (uint32_t it = 0; b < batch; b += groups, ++it) {
     const size_t boff = b * (size_t)K * Sh::Q;
+    st.phase = it & 1;
+    st.next_b = b + groups;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    split_round<W, LOGQ, LE, K, INV, PLO1, PW, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster);
+    split_round<W, LOGQ, LE, K, INV, PLO1, PW, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster, st);
+    if constexpr (INV) {
+      // after the epilogue's cluster barrier no CTA reads this buffer any more
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0 && st.next_b < batch)
+        split_issue_own<W, LOGQ, LE, K, INV>(st.map, st.next_b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
+    }
     __syncthreads();
   }
 }
@@ -214,7 +304,22 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   constexpr int LOGQ = LOGL - (K == 4 ? 2 : 1);
   constexpr int LE = SplitLE<W, K>::value;
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
-  const size_t smem = (size_t)Sh::Q * sizeof(W);
+  const size_t smem = (size_t)Sh::Q * sizeof(W) + (SplitStaging<W, LOGQ, LE, K, INV>::ON ? NTT_SMEM_ALIGN_SLACK + 64 : 0);
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  // 2-D tensor map of 128-byte rows over the array the first round reads its own block from
+  void* src = PW ? const_cast<void*>(pw.a) : x;
+  constexpr int ROW_WORDS = 128 / (int)sizeof(W);
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)ROW_WORDS, (cuuint64_t)(batch * K * (size_t)Sh::Q / ROW_WORDS)};
+  cuuint64_t strides[1] = {128};
+  constexpr int ROWS = Sh::Q / ROW_WORDS;
+  cuuint32_t box[2] = {(cuuint32_t)ROW_WORDS, (cuuint32_t)(ROWS < 256 ? ROWS : 256)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, src, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   auto kern = k_splitk<W, LOGQ, LE, K, INV, PLO1, PW>;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -244,8 +349,8 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<W*>(x), batch, reinterpret_cast<const TwPair<W>*>(tw),
-                            (W)p, pw);
+  return cudaLaunchKernelEx(&cfg, kern, map, reinterpret_cast<W*>(x), batch,
+                            reinterpret_cast<const TwPair<W>*>(tw), (W)p, pw);
 }
 
 // K = 2 is the default: measured faster than K = 4 (C3 1.44e12 vs 1.06e12 bfly/s, C4

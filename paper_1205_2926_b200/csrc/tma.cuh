@@ -7,6 +7,13 @@
 
 #include <cstdint>
 
+// Dynamic shared memory starts 1024-byte aligned on sm_100 (measured: base 0x400, after the
+// 1 KiB per-block reservation), which the 128-byte TMA swizzle needs; a kernel adds this
+// slack to its request only if it cannot rely on that.
+#ifndef NTT_SMEM_ALIGN_SLACK
+#define NTT_SMEM_ALIGN_SLACK 1024
+#endif
+
 namespace nttb {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
