@@ -143,9 +143,11 @@ struct ntt_plan_s {
   std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e table
   std::map<unsigned, void*> extra_sub_inv;  // log2 N -> omega_N^{-e} table
   // host-buffer executor (ntt_execute_host): pipeline streams and events
-  static constexpr int kSlots = 3;
-  cudaStream_t pipe[kSlots] = {nullptr, nullptr, nullptr};
-  cudaEvent_t pipe_done[kSlots] = {nullptr, nullptr, nullptr};
+  static constexpr int kSlots = 8;         // max pipeline slots (streams)
+  static constexpr int kDefaultSlots = 3;
+  static constexpr int kChunksPerSlot = 4;
+  cudaStream_t pipe[kSlots] = {};
+  cudaEvent_t pipe_done[kSlots] = {};
   cudaEvent_t start_ev = nullptr;
   // pointwise constants: K = beta mod p (plain) / beta L^{-1} mod p (scaled) and K'
   uint64_t K_plain = 0, Kp_plain = 0, K_scale = 0, Kp_scale = 0;
@@ -523,9 +525,22 @@ ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, vo
     }
   }
   // chunking: up to kSlots chunks resident in dev_buf, each >= 1 transform
-  const int slots = (int)std::min<size_t>(ntt_plan_s::kSlots, dev_buf_bytes / tbytes);
+  static int nslots = 0;
+  if (!nslots) {
+    const char* e = getenv("NTT_HOST_SLOTS");
+    nslots = (e && atoi(e) > 0) ? std::min(atoi(e), ntt_plan_s::kSlots) : ntt_plan_s::kDefaultSlots;
+  }
+  const int slots = (int)std::min<size_t>(nslots, dev_buf_bytes / tbytes);
   const size_t per_slot = dev_buf_bytes / slots / tbytes;        // transforms per chunk buffer
-  const size_t want = (batch + 4 * slots - 1) / (4 * slots);      // aim for >= 4 chunks per slot
+  // aim for >= kChunksPerSlot chunks per slot (shorter pipeline fill/drain; env override for
+  // experiments), but no chunk below ~1 MiB
+  static int cps = 0;
+  if (!cps) {
+    const char* e = getenv("NTT_HOST_CHUNKS_PER_SLOT");
+    cps = (e && atoi(e) > 0) ? atoi(e) : ntt_plan_s::kChunksPerSlot;
+  }
+  const size_t min_chunk = std::max<size_t>(1, ((size_t)1 << 20) / tbytes);
+  const size_t want = std::max(min_chunk, (batch + (size_t)cps * slots - 1) / ((size_t)cps * slots));
   const size_t chunk = std::max<size_t>(1, std::min(per_slot, want));
   cudaStream_t user = (cudaStream_t)stream;
   cudaError_t e = cudaEventRecord(pl->start_ev, user);
