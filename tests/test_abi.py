@@ -81,3 +81,31 @@ def test_pointer_checks_without_device(ntt):
     lib = ntt.lib()
     assert lib.ntt_forward(None, None, 1, None) == -1
     assert lib.ntt_synth_uniform(None, 10, 3, 0, 0, 0, 7, 0, None) == -1
+
+
+RNS = (469762049, 167772161, 998244353)
+
+
+def test_crt3_validation_without_device(ntt):
+    """ntt_crt3 (F3) checks its moduli and pointers before touching the device."""
+    lib = ntt.lib()
+    assert lib.ntt_crt3(None, None, None, None, 0, *RNS, None) == 0               # n = 0: no-op
+    assert lib.ntt_crt3(None, None, None, None, 5, *RNS, None) == -1              # null buffers
+    assert lib.ntt_crt3(None, None, None, None, 5, RNS[0], RNS[0], RNS[2], None) == -2  # equal primes
+    assert lib.ntt_crt3(None, None, None, None, 5, 998244351, RNS[1], RNS[2], None) == -2  # composite
+    assert lib.ntt_crt3(None, None, None, None, 5, 3221225473, RNS[1], RNS[2], None) == -2  # >= 2^30
+
+
+def test_block_transpose_validation_without_device(ntt):
+    lib = ntt.lib()
+    assert lib.ntt_block_transpose(None, None, 0, 4, 4, 8, None) == 0     # empty: no-op
+    assert lib.ntt_block_transpose(None, None, 2, 4, 4, 8, None) == -1    # null buffers
+    assert lib.ntt_block_transpose(16, 32, 2, 4, 4, 3, None) == -1        # word size
+    assert lib.ntt_block_transpose(16, 16, 2, 4, 4, 8, None) == -1        # aliasing
+    assert lib.ntt_block_transpose(16, 40, 2, 4, 4, 8, None) == -1        # misaligned source
+
+
+def test_fourstep_entry_points_reject_null_plan(ntt):
+    lib = ntt.lib()
+    assert lib.ntt_fourstep_cols_inv(None, 7, None, 0, 2, None) == -1
+    assert lib.ntt_fourstep_rows_inv(None, 7, None, None, 0, 2, None) == -1

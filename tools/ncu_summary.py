@@ -100,10 +100,43 @@ def launches(csv_path, out_md):
         agg[short][1] += v * scale
         total += v * scale
     lines = [f"# Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`): `{csv_path.split('/')[-1]}`",
-             "", "Cold-cache, serialised per-launch times: compare shares, not absolutes.", "",
+             "", "Cold-cache, serialised per-launch times: compare shares, not absolutes.  The whole bench command is",
+             "listed (ALU calibration, input generation, L2 flushes, the e2e host-pipeline chunks and the timed steps).", "",
              "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| `{k}` | {n} | {t:.1f} | {100 * t / total:.1f}% |")
+    # per (kernel, grid): the full-batch launches of the timed steps are the ones with the largest grid
+    gi = hdr.index("Grid Size") if "Grid Size" in hdr else None
+    if gi is not None:
+        byg = defaultdict(list)
+        for r in rows[1:]:
+            if len(r) <= vi or not r[vi]:
+                continue
+            v = float(r[vi].replace(",", ""))
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
+            byg[(r[ki].split("(")[0], r[gi])].append(v * scale)
+        lines += ["", "Per kernel and grid (mean per launch):", "", "| kernel | grid | launches | mean us |", "|---|---|---|---|"]
+        for (k, g), vs in sorted(byg.items(), key=lambda kv: -sum(kv[1])):
+            lines.append(f"| `{k}` | {g} | {len(vs)} | {sum(vs) / len(vs):.1f} |")
+    # launch sequence: consecutive launches of the same kernel and grid merged, in ID order, so the
+    # timed steps (warm-up + timed fwd/inv pairs) are visible apart from the e2e pipeline's chunks
+    lines += ["", "Launch sequence (consecutive identical kernels merged):", "",
+              "| first ID | kernel | grid | launches | us each |", "|---|---|---|---|---|"]
+    seq = []
+    for r in rows[1:]:
+        if len(r) <= vi or not r[vi]:
+            continue
+        v = float(r[vi].replace(",", ""))
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
+        key = (r[ki].split("(")[0].replace("void nttb::", "").replace("void ", ""), r[gi] if gi is not None else "")
+        us = round(v * scale, 1)
+        if seq and seq[-1][1] == key and abs(seq[-1][3][-1] - us) <= max(2.0, 0.1 * us):
+            seq[-1][3].append(us)
+        else:
+            seq.append([r[0], key, None, [us]])
+    for rid, (k, g), _, vs in seq:
+        each = f"{vs[0]:.1f}" if len(vs) == 1 else f"{min(vs):.1f}-{max(vs):.1f}"
+        lines.append(f"| {rid} | `{k[:70]}` | {g} | {len(vs)} | {each} |")
     open(out_md, "w").write("\n".join(lines) + "\n")
 
 
