@@ -142,6 +142,7 @@ def run_native(args, cfg, rank, world, local_rank):
     plans = [ntt.Plan(p, root(p, L), cfg["ell"], bits, device=local_rank) for p in cfg["primes"]]
     conv = cfg["ops"] == ("conv",)
     dist_c5 = cfg["key"] == "c5" and world > 1  # one transform split four-step over the ranks
+    exchange = None
     # inputs generated in HBM by the seeded counter-based generator (synth/ definition)
     seed = 0x12052926 ^ cfg["seed_cfg"]
     first = rank * batch
@@ -170,6 +171,29 @@ def run_native(args, cfg, rank, world, local_rank):
             recv = torch.empty_like(x)
             outbuf = torch.empty_like(x)
             fs = FourStepForward(plans[0], lay, rank)
+            # fused column pass + all-to-all over peer memory (ntt_fourstep_cols_p2p) when symmetric
+            # memory is available and its result matches the NCCL path on this input (checked once,
+            # outside the timed region); otherwise the NCCL all_to_all_single path
+            exchange, fs_p2p = "nccl", None
+            if os.environ.get("NTT_C5_EXCHANGE", "p2p") == "p2p":
+                try:
+                    from paper_1205_2926_b200.dist import FourStepForwardP2P
+                    import torch.distributed as dist
+                    fs_p2p = FourStepForwardP2P(plans[0], lay, rank)
+                    xa, xb_ = x0.clone(), x0.clone()
+                    oa, ob = torch.empty_like(x0), torch.empty_like(x0)
+                    fs_p2p(xa, oa, stream)
+                    fs(xb_, recv, ob, stream)
+                    ok = torch.tensor([1 if torch.equal(oa.view(torch.int64 if bits == 64 else torch.int32),
+                                                        ob.view(torch.int64 if bits == 64 else torch.int32)) else 0],
+                                      device=dev)
+                    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                    if int(ok.item()) == 1:
+                        exchange = "p2p"
+                    del xa, xb_, oa, ob
+                except Exception as exc:  # no symmetric memory / P2P on this system
+                    print(f"[bench] p2p exchange unavailable ({exc!r}); using NCCL all_to_all", file=sys.stderr)
+                    fs_p2p = None
         else:
             x0 = torch.empty(batch * L, dtype=dt, device=dev)
             ntt.synth_uniform(x0, seed, 0, start=first * L, bound=cfg["primes"][0], stream=stream)
@@ -182,8 +206,13 @@ def run_native(args, cfg, rank, world, local_rank):
         launches = 0
         if dist_c5:
             with torch.cuda.stream(stream):
-                for name, fn in (("cols", lambda: fs.cols(x, stream)), ("all_to_all", lambda: fs.exchange(x, recv)),
-                                 ("rows", lambda: fs.rows(recv, outbuf, stream))):
+                if exchange == "p2p":
+                    phases = (("cols+p2p_exchange", lambda: fs_p2p.cols_exchange(x, stream)),
+                              ("rows", lambda: fs_p2p.rows(outbuf, stream)))
+                else:
+                    phases = (("cols", lambda: fs.cols(x, stream)), ("all_to_all", lambda: fs.exchange(x, recv)),
+                              ("rows", lambda: fs.rows(recv, outbuf, stream)))
+                for name, fn in phases:
                     fn()
                     launches += ntt.last_launch_count() if name != "all_to_all" else 0
                     if evs is not None:
@@ -330,7 +359,10 @@ def run_native(args, cfg, rank, world, local_rank):
             e0.record(stream)
             with torch.cuda.stream(stream):
                 x.copy_(h_in, non_blocking=True)
-                fs(x, recv, outbuf, stream)
+                if exchange == "p2p":
+                    fs_p2p(x, outbuf, stream)
+                else:
+                    fs(x, recv, outbuf, stream)
                 h_out.copy_(outbuf, non_blocking=True)
             e1.record(stream)
             stream.synchronize()
@@ -341,7 +373,9 @@ def run_native(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": bfly_rank * world * len(ms) / (float(t.item()) * 1e-3), "unit": "butterflies/s",
                "h2d_bytes_per_step": x.numel() * wb, "d2h_bytes_per_step": x.numel() * wb,
-               "api": "pinned shard copies + FourStepForward (cols, NCCL all_to_all_single, rows)"}
+               "api": "pinned shard copies + " + ("FourStepForwardP2P (cols with fused P2P exchange, rows)"
+                                                   if exchange == "p2p" else
+                                                   "FourStepForward (cols, NCCL all_to_all_single, rows)")}
     elif not conv:
         ops = 0
         for op in cfg["ops"]:
@@ -403,7 +437,9 @@ def run_native(args, cfg, rank, world, local_rank):
             "data": "synthetic: seeded counter-based uniform residues generated in HBM (synth/ definition)",
             "config": {"workload": cfg["workload"], "transforms_per_gpu": batch, "L": L,
                        "butterflies_per_step_per_gpu": bfly_rank,
-                       "parallelism": (f"four-step split over {world} GPUs, one NCCL all_to_all" if dist_c5
+                       "parallelism": ((f"four-step split over {world} GPUs, all-to-all fused into the column pass "
+                                        "(P2P stores over NVLink, symmetric memory)" if exchange == "p2p" else
+                                        f"four-step split over {world} GPUs, one NCCL all_to_all") if dist_c5
                                        else f"batch-sharded x{world}, no collective"),
                        "passes": passes,
                        "l2": "flushed between timed steps (256 MiB zero-fill, outside the step events)"},

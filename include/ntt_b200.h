@@ -147,6 +147,19 @@ ntt_status ntt_fourstep_cols(ntt_plan_t plan, unsigned ell1, void* x_shard, unsi
 ntt_status ntt_fourstep_rows(ntt_plan_t plan, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,
                              ntt_stream_t stream);
 
+/* Fused compute + collective (SURVEY.md §8(e) "fused variant"): ntt_fourstep_cols with the
+ * all-to-all folded into its last column pass.  Instead of writing the shard in place, the
+ * pass stores row r of this rank's N1 x (N2/G) result straight into block `rank` of rank
+ * h = r / (N1/G)'s receive buffer, peer_recv[h] (device addresses valid on this device,
+ * e.g. symmetric-memory / P2P-mapped buffers of L/G words; peer_recv is a HOST array of
+ * `world` <= 8 addresses), over NVLink.  After every rank's call and a cross-rank barrier
+ * that orders these stores (stream-ordered, e.g. a symmetric-memory barrier), each
+ * rank's buffer holds exactly what all_to_all_single would have delivered, ready for
+ * ntt_fourstep_rows.  x_shard is used as scratch by the earlier column passes.
+ * NTT_ERR_UNSUPPORTED when the last column pass has no TMA-staged kernel (tiles > 64 KiB). */
+ntt_status ntt_fourstep_cols_p2p(ntt_plan_t plan, unsigned ell1, void* x_shard, const uint64_t* peer_recv,
+                                 unsigned rank, unsigned world, ntt_stream_t stream);
+
 /* ---- the same split run backwards, and layout helpers ----
  *   ntt_fourstep_rows_inv: `in` holds this rank's N1/G rows of Algorithm 1's
  *     bit-reversed output (flat positions [g L/G, (g+1) L/G), i.e. what

@@ -39,6 +39,14 @@ struct ColsParams {
   uint32_t log_local_w;    // log2 of the local matrix width (N2/G)
   uint32_t log_n2;         // log2 N2 (global width)
   uint32_t col0;           // first global column of this shard
+  // fused all-to-all (ntt_fourstep_cols_p2p, last column pass only): local row r goes to
+  // peer[r >> log_rows_rank] at word (src_rank << (log_rows_rank + log_local_w)) +
+  // ((r mod 2^log_rows_rank) << log_local_w) + local column, i.e. block src_rank of that
+  // rank's all-to-all receive buffer, written over NVLink instead of in place
+  uint32_t p2p;
+  uint32_t log_rows_rank;  // log2(N1/G)
+  uint32_t src_rank;
+  uint64_t peer[8];        // receive buffers of the G <= 8 ranks (device addresses)
 };
 
 struct DevTables {

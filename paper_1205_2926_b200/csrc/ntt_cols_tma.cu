@@ -160,7 +160,24 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
                                                bar_a[cur ^ 1], Sh::R > 1 && next < prm.n_tiles);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (prm.p2p) {
+      // fused all-to-all: every 16-byte chunk of the tile goes straight to the receive buffer of
+      // the rank that owns its row (peer memory over NVLink; the caller's cross-rank barrier
+      // orders these stores before the row pass reads them)
+      const uint64_t bq = tile >> prm.log_colgroups;
+      const uint32_t c0 = (uint32_t)(tile & cg_mask) * Sh::C, rmask = (1u << prm.log_rows_rank) - 1;
+      constexpr int PER = 16 / (int)sizeof(W);
+      for (int i = threadIdx.x; i < Sh::N * 8; i += Sh::THREADS) {
+        const int row = i >> 3, k = i & 7;
+        const uint4 val = lds128(reinterpret_cast<const unsigned char*>(sm) + row * 128 + ((k ^ (row & 7)) << 4));
+        const uint64_t r = bq * Sh::N + (uint64_t)row;  // global row (the last pass's blocks are N rows x N2/G)
+        W* dst = reinterpret_cast<W*>(prm.peer[r >> prm.log_rows_rank]) +
+                 ((uint64_t)prm.src_rank << (prm.log_rows_rank + prm.log_local_w)) +
+                 ((uint64_t)(r & rmask) << prm.log_local_w) + c0 + (uint32_t)k * PER;
+        *reinterpret_cast<uint4*>(dst) = val;
+      }
+      fence_proxy_async_smem();  // these generic reads precede the buffer's next TMA load
+    } else if (threadIdx.x == 0) {
       const int bq = (int)(tile >> prm.log_colgroups), c0 = (int)(tile & cg_mask) * Sh::C;
 #pragma unroll
       for (int bx = 0; bx < Sh::BOXES; ++bx)

@@ -622,7 +622,7 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, nt
 // Column half of the distributed four-step (forward: column NTTs then the twiddle;
 // inverse: the inverse twiddle then inverse column NTTs, passes in reverse order).
 static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
-                                     ntt_stream_t stream, bool inverse) {
+                                     ntt_stream_t stream, bool inverse, const uint64_t* peers = nullptr) {
   t_launches = 0;
   if (!pl || !x || !aligned16(x) || world == 0 || (world & (world - 1)) || rank >= world) return NTT_ERR_ARG;
   if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
@@ -666,6 +666,18 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
     prm.col0 = rank << log_wl;
     outer += logN;
   }
+  if (peers) {  // fused all-to-all: the last column pass scatters into the peers' receive buffers
+    if (world > 8) return NTT_ERR_UNSUPPORTED;
+    nttb::ColsParams& last = prms[nc - 1];
+    if (!tma_enabled() || !nttb::cols_tma_supported((int)pl->wbytes, (int)cp[nc - 1], last, x))
+      return NTT_ERR_UNSUPPORTED;
+    for (unsigned h = 0; h < world; ++h)
+      if (!peers[h] || (peers[h] & 15)) return NTT_ERR_ARG;
+    last.p2p = 1;
+    last.log_rows_rank = ell1 - lw;
+    last.src_rank = rank;
+    for (unsigned h = 0; h < world; ++h) last.peer[h] = peers[h];
+  }
   cudaError_t e = cudaSuccess;
   for (unsigned jj = 0; jj < nc && e == cudaSuccess; ++jj) {
     const unsigned j = inverse ? nc - 1 - jj : jj;
@@ -673,7 +685,8 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
     ntt_status st = sub_table(pl, cp[j], &sub, inverse);
     if (st != NTT_OK) return st;
     nttb::DevTables t{sub, sub, pl->fa, pl->fb};
-    e = launch_cols_any(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
+    e = prms[j].p2p ? nttb::launch_cols_tma(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream)
+                    : launch_cols_any(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
     ++t_launches;
   }
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
@@ -687,6 +700,12 @@ ntt_status ntt_fourstep_cols(ntt_plan_t pl, unsigned ell1, void* x, unsigned ran
 ntt_status ntt_fourstep_cols_inv(ntt_plan_t pl, unsigned ell1, void* x, unsigned rank, unsigned world,
                                  ntt_stream_t stream) {
   return fourstep_cols_impl(pl, ell1, x, rank, world, stream, true);
+}
+
+ntt_status ntt_fourstep_cols_p2p(ntt_plan_t pl, unsigned ell1, void* x, const uint64_t* peer_recv, unsigned rank,
+                                 unsigned world, ntt_stream_t stream) {
+  if (!peer_recv) { t_launches = 0; return NTT_ERR_ARG; }
+  return fourstep_cols_impl(pl, ell1, x, rank, world, stream, false, peer_recv);
 }
 
 ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, void* out, unsigned rank, unsigned world,

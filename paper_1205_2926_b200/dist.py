@@ -19,6 +19,10 @@ rank's rows of the bit-reversed spectrum, scattered straight into the all-to-all
 `FourStepInverseContig` take / return contiguous natural-order shards (rank g holds x[g L/G, (g+1) L/G))
 at the cost of a second all-to-all and one block transpose (`ntt_block_transpose`).
 
+`FourStepForwardP2P` fuses the all-to-all into the column pass (`ntt_fourstep_cols_p2p`): the last column
+pass stores each row straight into the owning rank's receive buffer over NVLink (torch symmetric memory gives
+the peer addresses and a stream-ordered cross-rank barrier), so no separate collective runs at all.
+
 The collective is `torch.distributed.all_to_all_single` on the NCCL process group (gloo in CPU tests);
 the compute steps are the CUDA kernels behind the C ABI (`Plan.fourstep_cols/rows`).  The layout
 helpers below are pure host logic, shared by the product path and the CPU tests.
@@ -191,4 +195,42 @@ class FourStepInverseContig:
         _exchange(buf, send, lay.world, self.inv.group)        # block g = rows [rank R, ...) x cols of rank g
         # G blocks of (rows x local_width) -> rows x (G blocks of local_width)
         block_transpose(out, send, lay.world, lay.rows_per_rank, lay.local_width, stream=stream)
+        return out
+
+
+class FourStepForwardP2P:
+    """FourStepForward with the all-to-all fused into the column pass over peer memory.
+
+    The receive buffer is a symmetric-memory allocation (torch.distributed._symmetric_memory) rendezvoused
+    on `group`; `peer_ptrs` are every rank's receive-buffer addresses as seen from this device.  One call:
+    ntt_fourstep_cols_p2p (column NTTs + twiddle, rows stored into the peers' buffers), a stream-ordered
+    symmetric-memory barrier, ntt_fourstep_rows.  `recv`/`peer_ptrs` may be passed in directly (tests run
+    G virtual ranks on one GPU with ordinary buffers and no barrier)."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None, recv=None, peer_ptrs=None, dtype=None):
+        self.plan, self.layout, self.rank, self.group = plan, layout, rank, group
+        self.hdl = None
+        if recv is None:
+            import torch
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            dt = dtype or (torch.uint64 if plan.word_bytes == 8 else torch.uint32)
+            self.recv = symm.empty(layout.shard_words, dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
+            self.hdl = symm.rendezvous(self.recv, group or dist.group.WORLD)
+            self.peer_ptrs = list(self.hdl.buffer_ptrs)
+        else:
+            self.recv, self.peer_ptrs = recv, list(peer_ptrs)
+
+    def cols_exchange(self, x_shard, stream=None):
+        self.plan.fourstep_cols_p2p(self.layout.ell1, x_shard, self.peer_ptrs, self.rank, self.layout.world,
+                                    stream=stream)
+        if self.hdl is not None:
+            self.hdl.barrier(channel=0)  # every rank's stores into this buffer are visible
+
+    def rows(self, out, stream=None):
+        self.plan.fourstep_rows(self.layout.ell1, self.recv, out, self.rank, self.layout.world, stream=stream)
+
+    def __call__(self, x_shard, out, stream=None):
+        self.cols_exchange(x_shard, stream)
+        self.rows(out, stream)
         return out

@@ -156,3 +156,68 @@ def test_block_transpose(ntt):
         dst = torch.empty_like(src)
         ntt.block_transpose(dst, src, n0, n1, n2)
         assert torch.equal(dst.view(n1, n0, n2), src.view(n0, n1, n2).transpose(0, 1))
+
+
+@pytest.mark.parametrize("p,bits,ell,ell1,G", [
+    (P62, 64, 12, 6, 2), (P62, 64, 16, 8, 4), (P30, 32, 16, 8, 2), (P62, 64, 20, 10, 8), (P62, 64, 28, 14, 8),
+])
+def test_fourstep_p2p_virtual_ranks(ntt, p, bits, ell, ell1, G):
+    """Fused column pass + all-to-all (ntt_fourstep_cols_p2p): G virtual ranks on one GPU whose 'peer'
+    receive buffers are local; after all ranks' column passes, the row pass output equals ntt_forward."""
+    from paper_1205_2926_b200.dist import FourStepForwardP2P, FourStepLayout
+    import synth
+    lay = FourStepLayout(ell, ell1, G)
+    L, N1, N2, Wl = lay.L, lay.N1, lay.N2, lay.local_width
+    w = pow(3, (p - 1) // L, p)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(5), 3, bound=p)
+    ref = x.clone()
+    plan.forward(ref)
+    shards = [x.view(N1, N2)[:, g * Wl:(g + 1) * Wl].contiguous().view(-1) for g in range(G)]
+    del x
+    recvs = [torch.full((lay.shard_words,), 7, dtype=dt, device="cuda") for _ in range(G)]
+    ptrs = [r.data_ptr() for r in recvs]
+    ranks = [FourStepForwardP2P(plan, lay, g, recv=recvs[g], peer_ptrs=ptrs) for g in range(G)]
+    for g in range(G):
+        ranks[g].cols_exchange(shards[g])
+    outs = []
+    for g in range(G):
+        o = torch.empty(lay.shard_words, dtype=dt, device="cuda")
+        ranks[g].rows(o)
+        outs.append(o)
+    assert _ieq(torch.cat(outs), ref, bits)
+
+
+def test_fourstep_p2p_symmetric_memory_world1(ntt):
+    """The product's P2P plumbing (torch symmetric memory rendezvous, peer pointers, stream-ordered barrier)
+    on a one-rank NCCL group: FourStepForwardP2P equals ntt_forward."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1205_2926_b200.dist import FourStepForwardP2P, FourStepLayout
+    import synth
+    if not dist.is_initialized():
+        sck = socket.socket()
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+        sck.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p, ell, ell1 = P62, 16, 8
+        lay = FourStepLayout(ell, ell1, 1)
+        plan = ntt.Plan(p, pow(3, (p - 1) >> ell, p), ell, 64)
+        x = torch.empty(lay.L, dtype=torch.uint64, device="cuda")
+        ntt.synth_uniform(x, synth.config_seed(5), 4, bound=p)
+        ref = x.clone()
+        plan.forward(ref)
+        fs = FourStepForwardP2P(plan, lay, 0)
+        out = torch.empty_like(x)
+        fs(x.clone(), out)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int64), ref.view(torch.int64))
+    finally:
+        dist.destroy_process_group()
