@@ -179,6 +179,13 @@ ntt_status ntt_fourstep_rows_inv(ntt_plan_t plan, unsigned ell1, const void* in,
                                  unsigned world, ntt_stream_t stream);
 ntt_status ntt_fourstep_cols_inv(ntt_plan_t plan, unsigned ell1, void* x_shard, unsigned rank, unsigned world,
                                  ntt_stream_t stream);
+/* ntt_fourstep_rows_inv with the all-to-all fused: block h of every row goes straight into
+ * block `rank` of rank h's receive buffer peer_recv[h] (peer memory over NVLink; HOST array of
+ * `world` <= 8 device addresses) instead of a local send buffer.  After every rank's call and
+ * a stream-ordered cross-rank barrier, each receive buffer is the column shard that
+ * ntt_fourstep_cols_inv takes. */
+ntt_status ntt_fourstep_rows_inv_p2p(ntt_plan_t plan, unsigned ell1, const void* in, const uint64_t* peer_recv,
+                                     unsigned rank, unsigned world, ntt_stream_t stream);
 
 /* Block transpose dst[j][i][k] = src[i][j][k] for i < n0, j < n1, k < n2 (words of
  * word_bytes = 4 or 8; device buffers, 16-byte aligned, not aliasing).  The pack /

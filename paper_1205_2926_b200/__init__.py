@@ -62,6 +62,7 @@ def _load() -> ctypes.CDLL:
         "ntt_fourstep_rows": [vp, uint, vp, vp, uint, uint, vp],
         "ntt_fourstep_cols_inv": [vp, uint, vp, uint, uint, vp],
         "ntt_fourstep_cols_p2p": [vp, uint, vp, ctypes.POINTER(u64), uint, uint, vp],
+        "ntt_fourstep_rows_inv_p2p": [vp, uint, vp, ctypes.POINTER(u64), uint, uint, vp],
         "ntt_fourstep_rows_inv": [vp, uint, vp, vp, uint, uint, vp],
         "ntt_block_transpose": [vp, vp, sz, sz, sz, uint, vp],
         "ntt_crt3": [vp, vp, vp, vp, sz, uint, uint, uint, vp],
@@ -87,7 +88,8 @@ _lib = _load()
 EXPORTED = (
     "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_pointwise_mul",
     "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
-    "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
+    "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p",
+    "ntt_fourstep_rows_inv_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
     "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
 )
 
@@ -216,6 +218,12 @@ class Plan:
         arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(q) for q in peer_ptrs])
         _check(_lib.ntt_fourstep_cols_p2p(self._h, ell1, _ptr(x_shard), arr, rank, world, _stream(stream)),
                "ntt_fourstep_cols_p2p")
+
+    def fourstep_rows_inv_p2p(self, ell1, x_rows, peer_ptrs, rank, world, stream=None):
+        """ntt_fourstep_rows_inv_p2p: peer_ptrs = the `world` receive-buffer device addresses (ints)."""
+        arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(q) for q in peer_ptrs])
+        _check(_lib.ntt_fourstep_rows_inv_p2p(self._h, ell1, _ptr(x_rows), arr, rank, world, _stream(stream)),
+               "ntt_fourstep_rows_inv_p2p")
 
     def fourstep_rows_inv(self, ell1, x_rows, send, rank, world, stream=None):
         _check(_lib.ntt_fourstep_rows_inv(self._h, ell1, _ptr(x_rows), _ptr(send), rank, world, _stream(stream)),

@@ -78,7 +78,8 @@ cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* rec
                                uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s);
 // distributed inverse (F4): inverse row NTTs, natural-order rows scattered into the send blocks
 cudaError_t launch_rows_scatter(int wbytes, int logn2, const void* in, void* send, uint32_t log_rows_local,
-                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s);
+                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s,
+                                const uint64_t* peers = nullptr, uint32_t src_rank = 0);
 cudaError_t launch_block_transpose(int wbytes, void* dst, const void* src, uint64_t n0, uint64_t n1, uint64_t n2,
                                    cudaStream_t s);
 // three-prime CRT (Garner), constants precomputed on the host (plan.cu, ntt_crt3)

@@ -47,6 +47,10 @@ struct GatherArgs {
   void* ext;                  // receive buffer (forward) / send buffer (inverse), or nullptr
   uint32_t log_w;             // log2(N2/G): width of one block
   uint32_t log_rows_local;    // log2(N1/G): rows per block
+  // inverse with the all-to-all fused (ntt_fourstep_rows_inv_p2p): block hb of row `row` goes to
+  // block src_rank of rank hb's receive buffer peer[hb] (peer memory over NVLink)
+  uint32_t p2p, src_rank;
+  uint64_t peer[8];
 };
 
 template <class W, int LOGN, int LE, bool INV, bool GATHER, bool PLO1, int r>
@@ -123,7 +127,11 @@ __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* 
             const int i = h * D + c[q];
             if constexpr (GATHER) {  // scatter: element i of row `row` -> block i >> log_w
               const int hb = i >> ga.log_w, off = i & ((1 << ga.log_w) - 1);
-              reinterpret_cast<W*>(ga.ext)[(((size_t)hb << ga.log_rows_local) + row) << ga.log_w | off] = v[q * S + h];
+              if (ga.p2p)
+                reinterpret_cast<W*>(ga.peer[hb])[(((size_t)ga.src_rank << ga.log_rows_local) + row) << ga.log_w | off] =
+                    v[q * S + h];
+              else
+                reinterpret_cast<W*>(ga.ext)[(((size_t)hb << ga.log_rows_local) + row) << ga.log_w | off] = v[q * S + h];
             } else {
               xb[i] = v[q * S + h];
             }
@@ -441,7 +449,7 @@ static cudaError_t cols_dispatch(int logn, void* x, const ColsParams& prm, const
 
 cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, void* x, size_t batch, const void* tw,
                           uint64_t p, cudaStream_t s) {
-  GatherArgs ga{nullptr, 0, 0};
+  GatherArgs ga{nullptr, 0, 0, 0u, 0u, {}};
   if (wbytes == 8) {
     return inverse ? contig_dispatch<uint64_t, true, false, 1, kContigMaxLog64>(logn, x, batch, tw, p, normalize, ga, s)
                    : contig_dispatch<uint64_t, false, false, 1, kContigMaxLog64>(logn, x, batch, tw, p, normalize, ga, s);
@@ -452,7 +460,7 @@ cudaError_t launch_contig(int wbytes, int logn, bool inverse, bool normalize, vo
 
 cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* recv, uint32_t log_rows_local,
                                uint32_t log_world, const void* tw, uint64_t p, cudaStream_t s) {
-  GatherArgs ga{const_cast<void*>(recv), (uint32_t)logn2 - log_world, log_rows_local};
+  GatherArgs ga{const_cast<void*>(recv), (uint32_t)logn2 - log_world, log_rows_local, 0u, 0u, {}};
   const size_t rows = (size_t)1 << log_rows_local;
   if (wbytes == 8)
     return contig_dispatch<uint64_t, false, true, 5, kContigMaxLog64>(logn2, out, rows, tw, p, true, ga, s);
@@ -460,8 +468,14 @@ cudaError_t launch_rows_gather(int wbytes, int logn2, void* out, const void* rec
 }
 
 cudaError_t launch_rows_scatter(int wbytes, int logn2, const void* in, void* send, uint32_t log_rows_local,
-                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s) {
-  GatherArgs ga{send, (uint32_t)logn2 - log_world, log_rows_local};
+                                uint32_t log_world, const void* tw_inv, uint64_t p, cudaStream_t s,
+                                const uint64_t* peers, uint32_t src_rank) {
+  GatherArgs ga{send, (uint32_t)logn2 - log_world, log_rows_local, 0u, 0u, {}};
+  if (peers) {
+    ga.p2p = 1;
+    ga.src_rank = src_rank;
+    for (uint32_t h = 0; h < (1u << log_world) && h < 8; ++h) ga.peer[h] = peers[h];
+  }
   const size_t rows = (size_t)1 << log_rows_local;
   void* x = const_cast<void*>(in);  // read only: the inverse's scatter writes to `send`
   if (wbytes == 8)

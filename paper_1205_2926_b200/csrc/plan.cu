@@ -733,11 +733,17 @@ ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, voi
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 
-ntt_status ntt_fourstep_rows_inv(ntt_plan_t pl, unsigned ell1, const void* in, void* send, unsigned rank,
-                                 unsigned world, ntt_stream_t stream) {
+static ntt_status fourstep_rows_inv_impl(ntt_plan_t pl, unsigned ell1, const void* in, void* send, unsigned rank,
+                                         unsigned world, ntt_stream_t stream, const uint64_t* peers) {
   t_launches = 0;
-  if (!pl || !in || !send || !aligned16(in) || in == send || world == 0 || (world & (world - 1)) || rank >= world)
+  if (!pl || !in || (!send && !peers) || !aligned16(in) || in == send || world == 0 || (world & (world - 1)) ||
+      rank >= world)
     return NTT_ERR_ARG;
+  if (peers) {
+    if (world > 8) return NTT_ERR_UNSUPPORTED;
+    for (unsigned h = 0; h < world; ++h)
+      if (!peers[h] || (peers[h] & 15)) return NTT_ERR_ARG;
+  }
   if (ell1 == 0 || ell1 >= pl->ell) return NTT_ERR_ARG;
   const unsigned ell2 = pl->ell - ell1;
   const unsigned cmax = pl->wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
@@ -750,9 +756,20 @@ ntt_status ntt_fourstep_rows_inv(ntt_plan_t pl, unsigned ell1, const void* in, v
   ntt_status st = sub_table(pl, ell2, &subi, true);
   if (st != NTT_OK) return st;
   cudaError_t e = nttb::launch_rows_scatter(pl->wbytes, (int)ell2, in, send, ell1 - lw, lw, subi, pl->p,
-                                            (cudaStream_t)stream);
+                                            (cudaStream_t)stream, peers, rank);
   ++t_launches;
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
+
+ntt_status ntt_fourstep_rows_inv(ntt_plan_t pl, unsigned ell1, const void* in, void* send, unsigned rank,
+                                 unsigned world, ntt_stream_t stream) {
+  return fourstep_rows_inv_impl(pl, ell1, in, send, rank, world, stream, nullptr);
+}
+
+ntt_status ntt_fourstep_rows_inv_p2p(ntt_plan_t pl, unsigned ell1, const void* in, const uint64_t* peer_recv,
+                                     unsigned rank, unsigned world, ntt_stream_t stream) {
+  if (!peer_recv) { t_launches = 0; return NTT_ERR_ARG; }
+  return fourstep_rows_inv_impl(pl, ell1, in, nullptr, rank, world, stream, peer_recv);
 }
 
 ntt_status ntt_block_transpose(void* dst, const void* src, size_t n0, size_t n1, size_t n2, unsigned word_bytes,

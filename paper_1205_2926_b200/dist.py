@@ -234,3 +234,39 @@ class FourStepForwardP2P:
         self.cols_exchange(x_shard, stream)
         self.rows(out, stream)
         return out
+
+
+class FourStepInverseP2P:
+    """FourStepInverse with the all-to-all fused into the row pass (ntt_fourstep_rows_inv_p2p): each row's
+    natural-order inverse is scattered straight into the owning ranks' receive buffers over NVLink, a
+    stream-ordered symmetric-memory barrier, then ntt_fourstep_cols_inv on this rank's buffer, which ends
+    as the natural-order column shard of L*a.  `recv`/`peer_ptrs` may be passed in (virtual-rank tests)."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None, recv=None, peer_ptrs=None, dtype=None):
+        self.plan, self.layout, self.rank = plan, layout, rank
+        self.hdl = None
+        if recv is None:
+            import torch
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            dt = dtype or (torch.uint64 if plan.word_bytes == 8 else torch.uint32)
+            self.recv = symm.empty(layout.shard_words, dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
+            self.hdl = symm.rendezvous(self.recv, group or dist.group.WORLD)
+            self.peer_ptrs = list(self.hdl.buffer_ptrs)
+        else:
+            self.recv, self.peer_ptrs = recv, list(peer_ptrs)
+
+    def rows_exchange(self, rows, stream=None):
+        self.plan.fourstep_rows_inv_p2p(self.layout.ell1, rows, self.peer_ptrs, self.rank, self.layout.world,
+                                        stream=stream)
+        if self.hdl is not None:
+            self.hdl.barrier(channel=0)
+
+    def cols_inv(self, stream=None):
+        self.plan.fourstep_cols_inv(self.layout.ell1, self.recv, self.rank, self.layout.world, stream=stream)
+
+    def __call__(self, rows, stream=None):
+        """Returns self.recv, which then holds the natural-order column shard of L*a."""
+        self.rows_exchange(rows, stream)
+        self.cols_inv(stream)
+        return self.recv

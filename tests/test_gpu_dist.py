@@ -221,3 +221,30 @@ def test_fourstep_p2p_symmetric_memory_world1(ntt):
         assert torch.equal(out.view(torch.int64), ref.view(torch.int64))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p,bits,ell,ell1,G", [(P62, 64, 16, 8, 4), (P30, 32, 16, 8, 2), (P62, 64, 28, 14, 8)])
+def test_fourstep_inverse_p2p_virtual_ranks(ntt, p, bits, ell, ell1, G):
+    """Fused row inverse + all-to-all (ntt_fourstep_rows_inv_p2p) then cols_inv: column shards of L*x."""
+    from paper_1205_2926_b200.dist import FourStepInverseP2P, FourStepLayout
+    import synth
+    lay = FourStepLayout(ell, ell1, G)
+    L, N1, N2, Wl = lay.L, lay.N1, lay.N2, lay.local_width
+    w = pow(3, (p - 1) // L, p)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(5), 5, bound=p)
+    spec = x.clone()
+    plan.forward(spec)
+    ref = spec.clone()
+    plan.inverse(ref)
+    recvs = [torch.full((lay.shard_words,), 9, dtype=dt, device="cuda") for _ in range(G)]
+    ptrs = [r.data_ptr() for r in recvs]
+    ranks = [FourStepInverseP2P(plan, lay, g, recv=recvs[g], peer_ptrs=ptrs) for g in range(G)]
+    for g in range(G):
+        ranks[g].rows_exchange(spec[g * lay.shard_words:(g + 1) * lay.shard_words])
+    for g in range(G):
+        ranks[g].cols_inv()
+        want = ref.view(N1, N2)[:, g * Wl:(g + 1) * Wl].contiguous().view(-1)
+        assert _ieq(recvs[g], want, bits), g
