@@ -32,4 +32,13 @@ __device__ __forceinline__ uint32_t cols_global_column(uint32_t cloc, const Cols
   return (rb << prm.log_n2) | (prm.col0 + cl);
 }
 
+// peer[h] without dynamic indexing of a kernel-parameter array (which would copy the whole
+// parameter struct to the stack): an unrolled select over the <= 8 entries.
+__device__ __forceinline__ uint64_t select_peer(const uint64_t (&peer)[8], uint32_t h) {
+  uint64_t d = peer[0];
+#pragma unroll
+  for (uint32_t i = 1; i < 8; ++i) d = (h == i) ? peer[i] : d;
+  return d;
+}
+
 }  // namespace nttb

@@ -120,7 +120,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
   }
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, bool P2P>
 __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaShape<W, LOGN, LE>::MINB)
     k_cols_tma(const __grid_constant__ CUtensorMap tmap, ColsParams prm, const TwPair<W>* __restrict__ tw,
                const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p) {
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
                                                bar_a[cur ^ 1], Sh::R > 1 && next < prm.n_tiles);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
-    if (prm.p2p) {
+    if constexpr (P2P) {
       // fused all-to-all: every 16-byte chunk of the tile goes straight to the receive buffer of
       // the rank that owns its row (peer memory over NVLink; the caller's cross-rank barrier
       // orders these stores before the row pass reads them)
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
         const int row = i >> 3, k = i & 7;
         const uint4 val = lds128(reinterpret_cast<const unsigned char*>(sm) + row * 128 + ((k ^ (row & 7)) << 4));
         const uint64_t r = bq * Sh::N + (uint64_t)row;  // global row (the last pass's blocks are N rows x N2/G)
-        W* dst = reinterpret_cast<W*>(prm.peer[r >> prm.log_rows_rank]) +
+        W* dst = reinterpret_cast<W*>(select_peer(prm.peer, (uint32_t)(r >> prm.log_rows_rank))) +
                  ((uint64_t)prm.src_rank << (prm.log_rows_rank + prm.log_local_w)) +
                  ((uint64_t)(r & rmask) << prm.log_local_w) + c0 + (uint32_t)k * PER;
         *reinterpret_cast<uint4*>(dst) = val;
@@ -193,7 +193,7 @@ template <class W, int LOGN> struct ColsTmaLE {
   static constexpr int value = sizeof(W) == 8 ? (LOGN < 4 ? LOGN : 4) : (LOGN < 5 ? LOGN : 5);
 };
 
-template <class W, int LOGN, bool INV, bool PLO1>
+template <class W, int LOGN, bool INV, bool PLO1, bool P2P>
 static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
   constexpr int LE = ColsTmaLE<W, LOGN>::value;
   using Sh = ColsTmaShape<W, LOGN, LE>;
@@ -209,7 +209,7 @@ static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables&
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1>;
+  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
@@ -232,10 +232,19 @@ static cudaError_t cols_tma_dispatch(int logn, void* x, const ColsParams& prm, c
     return cudaErrorInvalidValue;
   } else {
     if (logn == LO) {
+      // the fused all-to-all (p2p) epilogue is a separate instantiation, forward only
       if constexpr (sizeof(W) == 8) {
-        if ((p & 0xffffffffull) == 1) return run_cols_tma<W, LO, INV, true>(x, prm, tb, p, s);
+        if ((p & 0xffffffffull) == 1) {
+          if constexpr (!INV) {
+            if (prm.p2p) return run_cols_tma<W, LO, INV, true, true>(x, prm, tb, p, s);
+          }
+          return run_cols_tma<W, LO, INV, true, false>(x, prm, tb, p, s);
+        }
       }
-      return run_cols_tma<W, LO, INV, false>(x, prm, tb, p, s);
+      if constexpr (!INV) {
+        if (prm.p2p) return run_cols_tma<W, LO, INV, false, true>(x, prm, tb, p, s);
+      }
+      return run_cols_tma<W, LO, INV, false, false>(x, prm, tb, p, s);
     }
     return cols_tma_dispatch<W, INV, LO + 1, HI>(logn, x, prm, tb, p, s);
   }

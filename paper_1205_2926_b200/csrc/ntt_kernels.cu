@@ -128,7 +128,8 @@ __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* 
             if constexpr (GATHER) {  // scatter: element i of row `row` -> block i >> log_w
               const int hb = i >> ga.log_w, off = i & ((1 << ga.log_w) - 1);
               if (ga.p2p)
-                reinterpret_cast<W*>(ga.peer[hb])[(((size_t)ga.src_rank << ga.log_rows_local) + row) << ga.log_w | off] =
+                reinterpret_cast<W*>(select_peer(ga.peer, (uint32_t)hb))[(((size_t)ga.src_rank << ga.log_rows_local) + row)
+                                                                         << ga.log_w | off] =
                     v[q * S + h];
               else
                 reinterpret_cast<W*>(ga.ext)[(((size_t)hb << ga.log_rows_local) + row) << ga.log_w | off] = v[q * S + h];
