@@ -129,19 +129,22 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
   const uint32_t s0 = smem_u32(smem_raw);
   unsigned char* base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * (size_t)Sh::TILE_BYTES);
-  const uint32_t buf_a[2] = {smem_u32(base), smem_u32(base + Sh::TILE_BYTES)};
-  const uint32_t bar_a[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
+  // buffer / mbarrier of slot i by arithmetic, not a per-thread array (a dynamically indexed
+  // array would live on the stack)
+  const uint32_t buf0 = smem_u32(base), bar0 = smem_u32(&bars[0]);
+  auto buf_of = [&](int i) { return buf0 + (uint32_t)i * (uint32_t)Sh::TILE_BYTES; };
+  auto bar_of = [&](int i) { return bar0 + (uint32_t)i * 8u; };
   const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
   const Mod<W> m = make_mod<W>(p);
   const uint64_t cg_mask = (1ull << prm.log_colgroups) - 1;
   if (threadIdx.x == 0) {
-    mbar_init(bar_a[0], 1);
-    mbar_init(bar_a[1], 1);
+    mbar_init(bar_of(0), 1);
+    mbar_init(bar_of(1), 1);
     fence_mbar_init();
   }
   __syncthreads();
   uint64_t tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE>(&tmap, tile, prm.log_colgroups, buf_a[0], bar_a[0]);
+  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE>(&tmap, tile, prm.log_colgroups, buf_of(0), bar_of(0));
   W v[Sh::E];
   for (uint32_t it = 0; tile < prm.n_tiles; ++it, tile += gridDim.x) {
     const int cur = it & 1;
@@ -149,15 +152,15 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     if constexpr (Sh::R == 1) {  // no exchange to hide the prefetch behind: issue it now
       if (threadIdx.x == 0 && next < prm.n_tiles) {
         bulk_wait_read0();
-        cols_tma_issue<W, LOGN, LE>(&tmap, next, prm.log_colgroups, buf_a[cur ^ 1], bar_a[cur ^ 1]);
+        cols_tma_issue<W, LOGN, LE>(&tmap, next, prm.log_colgroups, buf_of(cur ^ 1), bar_of(cur ^ 1));
       }
     }
-    mbar_wait(bar_a[cur], (it >> 1) & 1);
+    mbar_wait(bar_of(cur), (it >> 1) & 1);
     const uint32_t cglob = cols_global_column((uint32_t)((tile & cg_mask) * Sh::C + cc), prm);
     W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_a[cur ^ 1],
-                                               bar_a[cur ^ 1], Sh::R > 1 && next < prm.n_tiles);
+    cols_tma_round<W, LOGN, LE, INV, PLO1, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_of(cur ^ 1),
+                                               bar_of(cur ^ 1), Sh::R > 1 && next < prm.n_tiles);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if constexpr (P2P) {
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
       const int bq = (int)(tile >> prm.log_colgroups), c0 = (int)(tile & cg_mask) * Sh::C;
 #pragma unroll
       for (int bx = 0; bx < Sh::BOXES; ++bx)
-        tma_store_3d(&tmap, c0, bx * Sh::BOX_ROWS, bq, buf_a[cur] + bx * Sh::BOX_ROWS * 128);
+        tma_store_3d(&tmap, c0, bx * Sh::BOX_ROWS, bq, buf_of(cur) + bx * Sh::BOX_ROWS * 128);
       bulk_commit();
     }
   }

@@ -150,41 +150,44 @@ __global__ void __launch_bounds__(TmaShape<W, LOGN, LE>::THREADS, TmaShape<W, LO
   const uint32_t s0 = smem_u32(smem_raw);
   unsigned char* base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * (size_t)Sh::TILE_BYTES);
-  const uint32_t buf_a[2] = {smem_u32(base), smem_u32(base + Sh::TILE_BYTES)};
-  const uint32_t bar_a[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
+  // buffer / mbarrier of slot i by arithmetic, not a per-thread array (a dynamically indexed
+  // array would live on the stack)
+  const uint32_t buf0 = smem_u32(base), bar0 = smem_u32(&bars[0]);
+  auto buf_of = [&](int i) { return buf0 + (uint32_t)i * (uint32_t)Sh::TILE_BYTES; };
+  auto bar_of = [&](int i) { return bar0 + (uint32_t)i * 8u; };
   const int slot = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
   const Mod<W> m = make_mod<W>(p);
   const size_t ntiles = (batch + Sh::K - 1) / Sh::K;
   if (threadIdx.x == 0) {
-    mbar_init(bar_a[0], 1);
-    mbar_init(bar_a[1], 1);
+    mbar_init(bar_of(0), 1);
+    mbar_init(bar_of(1), 1);
     fence_mbar_init();
   }
   __syncthreads();
   size_t tile = blockIdx.x;
   if (threadIdx.x == 0 && tile < ntiles) {
-    mbar_expect_tx(bar_a[0], Sh::TILE_BYTES);
+    mbar_expect_tx(bar_of(0), Sh::TILE_BYTES);
 #pragma unroll
     for (int bx = 0; bx < Sh::BOXES; ++bx)
-      tma_load_2d(buf_a[0] + bx * Sh::BOX_BYTES, &tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
-                  bar_a[0]);
+      tma_load_2d(buf_of(0) + bx * Sh::BOX_BYTES, &tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS,
+                  bar_of(0));
   }
   W v[Sh::E];
   for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     const int cur = it & 1;
-    mbar_wait(bar_a[cur], (it >> 1) & 1);
+    mbar_wait(bar_of(cur), (it >> 1) & 1);
     const size_t b = tile * Sh::K + slot;
     const bool active = b < batch;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
     W* sb = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES) + slot * Sh::N;  // stays in shared space
     tma_round<W, LOGN, LE, INV, PLO1, BF, r0>(v, x + b * Sh::N, sb, t, active, tw, m, norm != 0, true, &tmap,
-                                              tile + gridDim.x, ntiles, buf_a[cur ^ 1], bar_a[cur ^ 1]);
+                                              tile + gridDim.x, ntiles, buf_of(cur ^ 1), bar_of(cur ^ 1));
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if (threadIdx.x == 0) {  // rows past the tensor end (partial last tile) are clipped by TMA
 #pragma unroll
       for (int bx = 0; bx < Sh::BOXES; ++bx)
-        tma_store_2d(&tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS, buf_a[cur] + bx * Sh::BOX_BYTES);
+        tma_store_2d(&tmap, 0, (int)(tile * Sh::TILE_ROWS) + bx * Sh::BOX_ROWS, buf_of(cur) + bx * Sh::BOX_BYTES);
       bulk_commit();
     }
   }
