@@ -354,3 +354,23 @@ def test_config3_exact_integer_product(ntt):
         exact = np.convolve(ah[i].astype(np.int64), bh[i].astype(np.int64))
         assert np.array_equal(o[i, :2 * half - 1, 0].astype(np.int64), exact)
         assert (o[i, 2 * half - 1:, 0] == 0).all()
+
+
+@pytest.mark.parametrize("ell", [22, 24, 26])
+def test_u32_long_transforms(ntt, ell):
+    """beta = 2^32 up to the longest length its primes allow (p = 469762049 = 7*2^26+1, so 2^26): the
+    three-pass schedules.  Sampled outputs by Horner evaluation, inverse o forward = L x exactly."""
+    p = RNS[0]
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, 32)
+    x = torch.empty(L, dtype=torch.uint32, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(3), 7, bound=p)
+    xh = x.cpu().numpy().astype(np.uint64)
+    plan.forward(x)
+    fh = x.cpu().numpy().astype(np.uint64)
+    rng = np.random.default_rng(ell)
+    for j in [0, 1, L // 2, L - 1] + [int(v) for v in rng.integers(0, L, 4)]:
+        assert int(fh[j]) == oracle.ntt_output_at(p, w, xh, j), j
+    plan.inverse(x)
+    assert np.array_equal(x.cpu().numpy().astype(np.uint64), (xh * np.uint64(L)) % np.uint64(p))
