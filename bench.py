@@ -123,6 +123,62 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvmlSampler:
+    """SM clock and clock-event (throttle) reasons polled through NVML every ~1 ms on a thread, so
+    even a few-millisecond timed region is sampled (nvidia-smi's 100 ms period can miss it)."""
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, torch_device):
+        self.samples, self.reasons, self.h, self.nv = [], set(), None, None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            uuid = str(getattr(torch.cuda.get_device_properties(torch_device), "uuid", ""))
+            try:
+                self.h = nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(torch_device.index or 0)
+            self.nv = nv
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.h = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, const in self.NAMES:
+                    if r & getattr(nv, const, 0):
+                        self.reasons.add(name)
+            except Exception:
+                break
+            self._stop.wait(0.001)
+
+    def start(self):
+        if self.h is None:
+            return
+        self._stop = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        if self.h is None:
+            return None
+        self._stop.set()
+        self.t.join(timeout=2)
+        if not self.samples:
+            return None
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml, ~1 ms"}
+
+
 # ------------------------------------------------------------------ native arm
 def run_native(args, cfg, rank, world, local_rank):
     import torch
@@ -272,8 +328,10 @@ def run_native(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(local_rank)
     sampler.start()
+    nvml = NvmlSampler(dev)
     time.sleep(0.3)
     step_ms, kernel_ms, launches = [], {}, 0
+    nvml.start()  # exactly the timed region
     for _ in range(args.steps):
         reset_inputs()
         with torch.cuda.stream(stream):
@@ -291,7 +349,9 @@ def run_native(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    clocks = sampler.stop()
+    nv_clocks = nvml.stop()
+    smi_clocks = sampler.stop()
+    clocks = nv_clocks or smi_clocks
     clock_max = clocks.get("sm_max_mhz") or 1965.0
     alu_peak = derived_alu_peak(bits, p0, sms, clock_max)
     total_ms = sum(step_ms)
@@ -449,6 +509,7 @@ def run_native(args, cfg, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
+            "clocks_nvidia_smi": smi_clocks,
             "kernel_ms_mean": {k: round(statistics.mean(v), 4) for k, v in kernel_ms.items()},
         }
     return out
