@@ -205,6 +205,19 @@ void free_plan(ntt_plan_s* pl) {
 // transform fits; otherwise column passes of <= kColsMax stages followed by one
 // contiguous row pass of <= kContigMax stages, stage counts balanced.
 std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
+  // experiment hook: NTT_SCHEDULE="a,b[,c]" (outermost first, must sum to ell) overrides the schedule
+  if (const char* e = getenv("NTT_SCHEDULE")) {
+    std::vector<unsigned> s;
+    unsigned sum = 0;
+    for (const char* q = e; *q;) {
+      const unsigned v = (unsigned)strtoul(q, const_cast<char**>(&q), 10);
+      s.push_back(v);
+      sum += v;
+      if (*q == ',') ++q;
+      else if (*q) break;
+    }
+    if (sum == ell && !s.empty()) return s;
+  }
   const unsigned cmax = wbytes == 8 ? nttb::kContigMaxLog64 : nttb::kContigMaxLog32;
   const unsigned colmax = wbytes == 8 ? nttb::kColsMaxLog64 : nttb::kColsMaxLog32;
   // the contiguous pass reaches 2 * (on-chip max) on a 2-CTA cluster (ntt_split2.cu)
