@@ -143,11 +143,12 @@ struct ntt_plan_s {
   std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e table
   std::map<unsigned, void*> extra_sub_inv;  // log2 N -> omega_N^{-e} table
   // host-buffer executor (ntt_execute_host): pipeline streams and events
-  static constexpr int kSlots = 8;         // max pipeline slots (streams)
-  static constexpr int kDefaultSlots = 3;
-  static constexpr int kChunksPerSlot = 4;
-  cudaStream_t pipe[kSlots] = {};
-  cudaEvent_t pipe_done[kSlots] = {};
+  static constexpr int kRing = 8;           // max device buffers in the host pipeline's ring
+  static constexpr int kDefaultRing = 4;
+  static constexpr int kDefaultChunks = 8;
+  cudaStream_t pipe[3] = {};                 // H2D, compute, D2H
+  cudaEvent_t pipe_done[3] = {};
+  cudaEvent_t ring_ev[3 * kRing] = {};       // loaded / computed / freed per ring buffer
   cudaEvent_t start_ev = nullptr;
   // pointwise constants: K = beta mod p (plain) / beta L^{-1} mod p (scaled) and K'
   uint64_t K_plain = 0, Kp_plain = 0, K_scale = 0, Kp_scale = 0;
@@ -192,10 +193,12 @@ void free_plan(ntt_plan_s* pl) {
   {
     DeviceGuard g(pl->device);
     for (void* d : pl->owned) cudaFree(d);
-    for (int i = 0; i < ntt_plan_s::kSlots; ++i) {
+    for (int i = 0; i < 3; ++i) {
       if (pl->pipe[i]) cudaStreamDestroy(pl->pipe[i]);
       if (pl->pipe_done[i]) cudaEventDestroy(pl->pipe_done[i]);
     }
+    for (int i = 0; i < 3 * ntt_plan_s::kRing; ++i)
+      if (pl->ring_ev[i]) cudaEventDestroy(pl->ring_ev[i]);
     if (pl->start_ev) cudaEventDestroy(pl->start_ev);
   }
   delete pl;
@@ -516,6 +519,11 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 
+// Host-buffer pipeline: three role streams -- H2D copies, transforms, D2H copies -- over a ring of
+// NB device buffers carved from dev_buf.  Chunk k uses buffer k mod NB; its H2D waits until the
+// D2H of chunk k - NB has drained that buffer, so both copy directions stay busy back to back
+// (C2 end to end: 3.33 ms vs 3.46 ms for per-chunk streams doing all three stages; the copies
+// alone pipeline in 3.06 ms, tools/e2e_probe.py).
 ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, void* host_out, size_t batch,
                             void* dev_buf, size_t dev_buf_bytes, ntt_stream_t stream) {
   if (!pl || !ops || (ops & ~(NTT_OP_FORWARD | NTT_OP_INVERSE))) return NTT_ERR_ARG;
@@ -525,62 +533,76 @@ ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, vo
   const size_t tbytes = (size_t)L * pl->wbytes;
   if (batch > SIZE_MAX / tbytes || dev_buf_bytes < tbytes) return NTT_ERR_ARG;
   DeviceGuard g(pl->device);
+  using P = ntt_plan_s;
   {
     std::lock_guard<std::mutex> lk(pl->mu);
     if (!pl->start_ev) {
-      for (int i = 0; i < ntt_plan_s::kSlots; ++i) {
+      for (int i = 0; i < 3; ++i) {
         cudaError_t e = cudaStreamCreateWithFlags(&pl->pipe[i], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->pipe_done[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e);
+      }
+      for (int i = 0; i < 3 * P::kRing; ++i) {
+        cudaError_t e = cudaEventCreateWithFlags(&pl->ring_ev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e);
+      }
+      for (int i = 0; i < 3; ++i) {
+        cudaError_t e = cudaEventCreateWithFlags(&pl->pipe_done[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e);
       }
       cudaError_t e = cudaEventCreateWithFlags(&pl->start_ev, cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_fail(e);
     }
   }
-  // chunking: up to kSlots chunks resident in dev_buf, each >= 1 transform
-  static int nslots = 0;
-  if (!nslots) {
-    const char* e = getenv("NTT_HOST_SLOTS");
-    nslots = (e && atoi(e) > 0) ? std::min(atoi(e), ntt_plan_s::kSlots) : ntt_plan_s::kDefaultSlots;
+  static int env_nb = -1, env_chunks = -1;
+  if (env_nb < 0) {
+    const char* e1 = getenv("NTT_HOST_RING");
+    const char* e2 = getenv("NTT_HOST_CHUNKS");
+    env_nb = (e1 && atoi(e1) > 0) ? std::min(atoi(e1), P::kRing) : P::kDefaultRing;
+    env_chunks = (e2 && atoi(e2) > 0) ? atoi(e2) : P::kDefaultChunks;
   }
-  const int slots = (int)std::min<size_t>(nslots, dev_buf_bytes / tbytes);
-  const size_t per_slot = dev_buf_bytes / slots / tbytes;        // transforms per chunk buffer
-  // aim for >= kChunksPerSlot chunks per slot (shorter pipeline fill/drain; env override for
-  // experiments), but no chunk below ~1 MiB
-  static int cps = 0;
-  if (!cps) {
-    const char* e = getenv("NTT_HOST_CHUNKS_PER_SLOT");
-    cps = (e && atoi(e) > 0) ? atoi(e) : ntt_plan_s::kChunksPerSlot;
-  }
+  // ring of NB buffers of `chunk` transforms each; aim for env_chunks chunks, none below ~1 MiB
+  const int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)env_nb, dev_buf_bytes / tbytes));
+  const size_t per_buf = dev_buf_bytes / nb / tbytes;
   const size_t min_chunk = std::max<size_t>(1, ((size_t)1 << 20) / tbytes);
-  const size_t want = std::max(min_chunk, (batch + (size_t)cps * slots - 1) / ((size_t)cps * slots));
-  const size_t chunk = std::max<size_t>(1, std::min(per_slot, want));
+  const size_t want = std::max(min_chunk, (batch + (size_t)env_chunks - 1) / (size_t)env_chunks);
+  const size_t chunk = std::max<size_t>(1, std::min(per_buf, want));
   cudaStream_t user = (cudaStream_t)stream;
+  cudaStream_t h2d = pl->pipe[0], comp = pl->pipe[1], d2h = pl->pipe[2];
+  cudaEvent_t* loaded = pl->ring_ev;
+  cudaEvent_t* computed = pl->ring_ev + P::kRing;
+  cudaEvent_t* freed = pl->ring_ev + 2 * P::kRing;
   cudaError_t e = cudaEventRecord(pl->start_ev, user);
-  for (int i = 0; e == cudaSuccess && i < slots; ++i) e = cudaStreamWaitEvent(pl->pipe[i], pl->start_ev, 0);
+  for (int i = 0; e == cudaSuccess && i < 3; ++i) e = cudaStreamWaitEvent(pl->pipe[i], pl->start_ev, 0);
   if (e != cudaSuccess) return cuda_fail(e);
   unsigned launches = 0;
-  int k = 0;
-  for (size_t b0 = 0; b0 < batch; b0 += chunk, k = (k + 1) % slots) {
-    const size_t nb = std::min(chunk, batch - b0);
-    void* d = (uint8_t*)dev_buf + (size_t)k * per_slot * tbytes;
-    cudaStream_t s = pl->pipe[k];
-    e = cudaMemcpyAsync(d, (const uint8_t*)host_in + b0 * tbytes, nb * tbytes, cudaMemcpyHostToDevice, s);
+  size_t k = 0;
+  for (size_t b0 = 0; b0 < batch; b0 += chunk, ++k) {
+    const size_t n = std::min(chunk, batch - b0);
+    const int b = (int)(k % (size_t)nb);
+    void* d = (uint8_t*)dev_buf + (size_t)b * per_buf * tbytes;
+    if (k >= (size_t)nb && (e = cudaStreamWaitEvent(h2d, freed[b], 0)) != cudaSuccess) return cuda_fail(e);
+    e = cudaMemcpyAsync(d, (const uint8_t*)host_in + b0 * tbytes, n * tbytes, cudaMemcpyHostToDevice, h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(loaded[b], h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, loaded[b], 0);
     if (e != cudaSuccess) return cuda_fail(e);
     if (ops & NTT_OP_FORWARD) {
-      ntt_status st = run_transform(pl, d, nb, s, false);
+      ntt_status st = run_transform(pl, d, n, comp, false);
       launches += t_launches;
       if (st != NTT_OK) return st;
     }
     if (ops & NTT_OP_INVERSE) {
-      ntt_status st = run_transform(pl, d, nb, s, true);
+      ntt_status st = run_transform(pl, d, n, comp, true);
       launches += t_launches;
       if (st != NTT_OK) return st;
     }
-    e = cudaMemcpyAsync((uint8_t*)host_out + b0 * tbytes, d, nb * tbytes, cudaMemcpyDeviceToHost, s);
+    e = cudaEventRecord(computed[b], comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, computed[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((uint8_t*)host_out + b0 * tbytes, d, n * tbytes, cudaMemcpyDeviceToHost, d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(freed[b], d2h);
     if (e != cudaSuccess) return cuda_fail(e);
   }
-  for (int i = 0; e == cudaSuccess && i < slots; ++i) {
+  for (int i = 0; e == cudaSuccess && i < 3; ++i) {
     e = cudaEventRecord(pl->pipe_done[i], pl->pipe[i]);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(user, pl->pipe_done[i], 0);
   }

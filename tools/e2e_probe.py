@@ -58,3 +58,63 @@ for mb in (32, 64, 128, 256):
     ms = timed(lambda: plan.execute_host(ntt.NTT_OP_FORWARD | ntt.NTT_OP_INVERSE, h_in, h_out, buf))
     res[f"execute_host_{mb}MiB_ms"] = round(ms, 3)
 print({k: round(v, 2) for k, v in res.items()})
+
+# pure-copy pipeline with the same chunking as ntt_execute_host (3 streams, 12 chunks): the PCIe floor
+streams = [torch.cuda.Stream() for _ in range(3)]
+chunks = 12
+cw = n // chunks
+bufs = [torch.empty(cw, dtype=torch.uint64, device="cuda") for _ in range(3)]
+
+
+def pipe():
+    ev = torch.cuda.Event()
+    ev.record(s)
+    for st in streams:
+        st.wait_event(ev)
+    for k in range(chunks):
+        st = streams[k % 3]
+        with torch.cuda.stream(st):
+            bufs[k % 3].copy_(h_in[k * cw:(k + 1) * cw], non_blocking=True)
+            h_out[k * cw:(k + 1) * cw].copy_(bufs[k % 3], non_blocking=True)
+    for st in streams:
+        e = torch.cuda.Event()
+        e.record(st)
+        s.wait_event(e)
+
+
+print({"copy_only_pipeline_ms": round(timed(pipe), 3)})
+
+# role-split pipeline: one H2D stream, one D2H stream, a ring of NB buffers (copies only)
+def role_pipe(nb, chunks):
+    cw = n // chunks
+    ring = [torch.empty(cw, dtype=torch.uint64, device="cuda") for _ in range(nb)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    freed = [None] * nb
+
+    def run():
+        ev = torch.cuda.Event()
+        ev.record(s)
+        h2d_s.wait_event(ev)
+        d2h_s.wait_event(ev)
+        for k in range(chunks):
+            b = k % nb
+            if freed[b] is not None:
+                h2d_s.wait_event(freed[b])
+            with torch.cuda.stream(h2d_s):
+                ring[b].copy_(h_in[k * cw:(k + 1) * cw], non_blocking=True)
+            loaded = torch.cuda.Event()
+            loaded.record(h2d_s)
+            d2h_s.wait_event(loaded)
+            with torch.cuda.stream(d2h_s):
+                h_out[k * cw:(k + 1) * cw].copy_(ring[b], non_blocking=True)
+            fe = torch.cuda.Event()
+            fe.record(d2h_s)
+            freed[b] = fe
+        e = torch.cuda.Event()
+        e.record(d2h_s)
+        s.wait_event(e)
+    return run
+
+
+for nb, ch in ((4, 16),):
+    print({f"role_pipe_nb{nb}_ch{ch}_ms": round(timed(role_pipe(nb, ch)), 3)})
