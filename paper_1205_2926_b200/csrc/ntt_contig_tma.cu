@@ -69,9 +69,6 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
   }
   constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
   // ---- load from the swizzled tile buffer
-#ifdef NTT_EXP_NOEXCH2  // timing experiment only (wrong results): later rounds keep their registers
-  if (r == (INV ? Sh::R - 1 : 0))
-#endif
 #pragma unroll
   for (int q = 0; q < G; ++q) {
     if constexpr (VEC) {
@@ -119,7 +116,6 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
         tma_load_2d(next_buf + bx * Sh::BOX_BYTES, map, 0, row0 + bx * Sh::BOX_ROWS, next_bar);
     }
     // ---- exchange (same positions as this round's load)
-#if !defined(NTT_EXP_NOEXCH) && !defined(NTT_EXP_NOEXCH2)  // timing experiments only (wrong results)
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       if constexpr (VEC) {
@@ -132,7 +128,6 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
       }
     }
     __syncthreads();
-#endif
     constexpr int nr = INV ? r - 1 : r + 1;
     tma_round<W, LOGN, LE, INV, PLO1, BF, nr>(v, xb, sb, t, active, tw, m, norm, false, map, next_tile, ntiles,
                                               next_buf, next_bar);

@@ -65,17 +65,9 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
 #pragma unroll
       for (int hh = 0; hh < half; ++hh) {
         // k = hh*D + c; when D == 1 (c == 0) the hh == 0 butterflies have k = 0, i.e. W = 1
-#ifdef NTT_EXP_NOMUL  // timing experiment only (wrong results): every butterfly multiply-free
-        const bool unit = true;
-#else
         const bool unit = w1 || (D == 1 && hh == 0);
-#endif
         W w = 1, wp = 0;
-#ifdef NTT_EXP_NOTW  // timing experiment only (wrong results): no twiddle loads
-        if (!unit) { w = (W)(off + hh * D + c[q]) * 3 + 5; wp = w * 7; }
-#else
         if (!unit) ldtw<W>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
-#endif
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
