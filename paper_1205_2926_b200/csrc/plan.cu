@@ -207,6 +207,8 @@ void free_plan(ntt_plan_s* pl) {
 // Pass schedule: one on-chip pass when the
 // transform fits; otherwise column passes of <= kColsMax stages followed by one
 // contiguous row pass of <= kContigMax stages, stage counts balanced.
+constexpr unsigned kRowPassLog64 = 12;  // row pass of >= 3-pass beta = 2^64 schedules
+
 std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
   // experiment hook: NTT_SCHEDULE="a,b[,c]" (outermost first, must sum to ell) overrides the schedule
   if (const char* e = getenv("NTT_SCHEDULE")) {
@@ -229,6 +231,15 @@ std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
     const unsigned col = std::min(colmax, ell / np);
     const unsigned last = ell - col * (np - 1);
     if (last <= cmax + 1) {
+      if (np >= 3 && wbytes == 8 && ell - kRowPassLog64 <= (np - 1) * colmax) {
+        // three or more passes: a 2^12 row pass in the TMA-staged kernel and balanced column
+        // passes, larger first (measured C5 2^28: [8,8,12] 6.90 ms vs [9,9,10] 7.28 ms)
+        const unsigned rest = ell - kRowPassLog64, nc = np - 1;
+        std::vector<unsigned> s(np, rest / nc);
+        for (unsigned i = 0; i < rest % nc; ++i) s[i] += 1;
+        s[np - 1] = kRowPassLog64;
+        if (s[nc - 1] >= (unsigned)nttb::kColsMinLog) return s;
+      }
       std::vector<unsigned> s(np, col);
       s[np - 1] = last;
       return s;

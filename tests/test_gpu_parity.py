@@ -374,3 +374,27 @@ def test_u32_long_transforms(ntt, ell):
         assert int(fh[j]) == oracle.ntt_output_at(p, w, xh, j), j
     plan.inverse(x)
     assert np.array_equal(x.cpu().numpy().astype(np.uint64), (xh * np.uint64(L)) % np.uint64(p))
+
+
+@pytest.mark.parametrize("ell", [25, 27])
+def test_u64_three_pass_lengths(ntt, ell):
+    """beta = 2^64 lengths with three-pass schedules ([7,6,12], [8,7,12]): Horner-sampled outputs and
+    inverse o forward = L x on a 2^17-position sample."""
+    p = P62
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, 64)
+    info = plan.info()
+    assert info.n_passes == 3
+    x = torch.empty(L, dtype=torch.uint64, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(4), 9, bound=p)
+    xh = x.cpu().numpy()
+    plan.forward(x)
+    fh = x.cpu().numpy()
+    rng = np.random.default_rng(ell)
+    for j in [0, 1, L - 1] + [int(v) for v in rng.integers(0, L, 3)]:
+        assert int(fh[j]) == oracle.ntt_output_at(p, w, xh, j), j
+    plan.inverse(x)
+    ih = x.cpu().numpy()
+    idx = rng.integers(0, L, 1 << 17)
+    assert all(int(ih[i]) == int(xh[i]) * L % p for i in idx)
