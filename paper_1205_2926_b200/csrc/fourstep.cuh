@@ -25,6 +25,24 @@ __device__ __forceinline__ W fourstep_twiddle(W val, uint32_t e, const ColsParam
   return shoup_mul<W, PLO1>(val, w, wp, m);
 }
 
+// The same with the table form fixed at compile time (FACT: factored, two Shoup multiplies), so
+// a kernel's per-element twiddle code has no branch and its loads can be scheduled early.
+template <class W, bool PLO1, bool FACT>
+__device__ __forceinline__ W fourstep_twiddle_ct(W val, uint32_t e, uint32_t H, const TwPair<W>* __restrict__ fa,
+                                                 const TwPair<W>* __restrict__ fb, const Mod<W>& m) {
+  W w, wp;
+  if constexpr (!FACT) {
+    ldtw<W>(fa, e, w, wp);
+    return shoup_mul<W, PLO1>(val, w, wp, m);
+  } else {
+    W w2, wp2;
+    ldtw<W>(fb, e & ((1u << H) - 1), w, wp);
+    ldtw<W>(fa, e >> H, w2, wp2);
+    val = shoup_mul<W, PLO1>(val, w, wp, m);
+    return shoup_mul<W, PLO1>(val, w2, wp2, m);
+  }
+}
+
 // Global column of local column `cloc` (ColsParams.shard: config C5 column shard).
 __device__ __forceinline__ uint32_t cols_global_column(uint32_t cloc, const ColsParams& prm) {
   if (!prm.shard) return cloc;

@@ -47,7 +47,7 @@ __device__ __forceinline__ void cols_tma_issue(const CUtensorMap* map, uint64_t 
   for (int bx = 0; bx < Sh::BOXES; ++bx) tma_load_3d(buf + bx * Sh::BOX_ROWS * 128, map, c0, bx * Sh::BOX_ROWS, bq, bar);
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1, int r>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, bool FACT, int r>
 __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint32_t cglob, const ColsParams& prm,
                                                const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
                                                const TwPair<W>* __restrict__ fb, const Mod<W>& m,
@@ -73,17 +73,22 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      W val = sm[tswz<W>(row * C + cc)];
-      if constexpr (INV && first) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
-        if (prm.twiddle) {
+      v[q * S + h] = sm[tswz<W>(row * C + cc)];
+    }
+  if constexpr (INV && first) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
+    if (prm.twiddle) {
+      const uint32_t emask = (uint32_t)((((uint64_t)1 << prm.ell)) - 1);
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int h = 0; h < S; ++h) {
+          const int row = blk[q] * B + h * D + c[q];
           const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
           const uint32_t e = (cglob * rv) << prm.log_tw_mul;
-          const uint32_t einv = (uint32_t)((((uint64_t)1 << prm.ell) - e) & (((uint64_t)1 << prm.ell) - 1));
-          val = fourstep_twiddle<W, PLO1>(val, einv, prm, fa, fb, m);
+          v[q * S + h] = fourstep_twiddle_ct<W, PLO1, FACT>(v[q * S + h], (0u - e) & emask, prm.H, fa, fb, m);
         }
-      }
-      v[q * S + h] = val;
     }
+  }
   if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (!last) {
@@ -93,34 +98,46 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
       cols_tma_issue<W, LOGN, LE>(map, next_tile, prm.log_colgroups, next_buf, next_bar);
     }
   }
+  if constexpr (last) {
+    if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
+      if (prm.twiddle) {
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; ++h) {
+            const int row = blk[q] * B + h * D + c[q];
+            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+            v[q * S + h] = fourstep_twiddle_ct<W, PLO1, FACT>(v[q * S + h], (cglob * rv) << prm.log_tw_mul, prm.H, fa,
+                                                              fb, m);
+          }
+      }
+      if (prm.normalize) {
+#pragma unroll
+        for (int i = 0; i < Sh::E; ++i) v[i] = norm2<W>(v[i], m.p);
+      }
+    } else {
+      if (prm.normalize) {
+#pragma unroll
+        for (int i = 0; i < Sh::E; ++i) v[i] = norm4<W>(v[i], m.p, m.p2);
+      }
+    }
+  }
 #pragma unroll
   for (int q = 0; q < G; ++q)
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      W val = v[q * S + h];
-      if constexpr (last) {
-        if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
-          if (prm.twiddle) {
-            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
-            val = fourstep_twiddle<W, PLO1>(val, (cglob * rv) << prm.log_tw_mul, prm, fa, fb, m);
-          }
-          if (prm.normalize) val = norm2<W>(val, m.p);
-        } else {
-          if (prm.normalize) val = norm4<W>(val, m.p, m.p2);
-        }
-      }
-      sm[tswz<W>(row * C + cc)] = val;  // each thread rewrites exactly the positions it read
+      sm[tswz<W>(row * C + cc)] = v[q * S + h];  // each thread rewrites exactly the positions it read
     }
   if constexpr (!last) {
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, map, next_tile, next_buf,
-                                               next_bar, false);
+    cols_tma_round<W, LOGN, LE, INV, PLO1, FACT, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, map, next_tile,
+                                                     next_buf, next_bar, false);
   }
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1, bool P2P>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, bool P2P, bool FACT>
 __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaShape<W, LOGN, LE>::MINB)
     k_cols_tma(const __grid_constant__ CUtensorMap tmap, ColsParams prm, const TwPair<W>* __restrict__ tw,
                const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p) {
@@ -159,7 +176,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     const uint32_t cglob = cols_global_column((uint32_t)((tile & cg_mask) * Sh::C + cc), prm);
     W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_of(cur ^ 1),
+    cols_tma_round<W, LOGN, LE, INV, PLO1, FACT, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_of(cur ^ 1),
                                                bar_of(cur ^ 1), Sh::R > 1 && next < prm.n_tiles);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
@@ -196,8 +213,8 @@ template <class W, int LOGN> struct ColsTmaLE {
   static constexpr int value = sizeof(W) == 8 ? (LOGN < 4 ? LOGN : 4) : (LOGN < 5 ? LOGN : 5);
 };
 
-template <class W, int LOGN, bool INV, bool PLO1, bool P2P>
-static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
+template <class W, int LOGN, bool INV, bool PLO1, bool P2P, bool FACT>
+static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
   constexpr int LE = ColsTmaLE<W, LOGN>::value;
   using Sh = ColsTmaShape<W, LOGN, LE>;
   auto enc = encode_fn();
@@ -212,7 +229,7 @@ static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables&
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P>;
+  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, FACT>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
@@ -226,6 +243,12 @@ static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables&
                                            reinterpret_cast<const TwPair<W>*>(tb.fa),
                                            reinterpret_cast<const TwPair<W>*>(tb.fb), (W)p);
   return cudaGetLastError();
+}
+
+template <class W, int LOGN, bool INV, bool PLO1, bool P2P>
+static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
+  if (prm.H) return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, true>(x, prm, tb, p, s);
+  return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, false>(x, prm, tb, p, s);
 }
 
 template <class W, bool INV, int LO, int HI>

@@ -275,6 +275,10 @@ ntt_status build_fourstep_tables(ntt_plan_s* pl) {
     pl->fb = pl->fa;
   } else {
     pl->H = (pl->ell + 1) / 2;
+    if (const char* e = getenv("NTT_FOURSTEP_H")) {  // experiment hook
+      const unsigned h = (unsigned)atoi(e);
+      if (h >= 1 && h < pl->ell) pl->H = h;
+    }
     st = upload(pl, make_table(pl->p, powmod(pl->omega, (uint64_t)1 << pl->H, pl->p), L >> pl->H, pl->bits), &pl->fa);
     if (st == NTT_OK) st = upload(pl, make_table(pl->p, pl->omega, (uint64_t)1 << pl->H, pl->bits), &pl->fb);
   }
