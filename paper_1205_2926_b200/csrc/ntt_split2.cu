@@ -126,7 +126,34 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   if constexpr (first) {
     // inverse: this CTA's block of the transform has been staged in shared memory
     if constexpr (INV) mbar_wait(split_bar<W, LOGQ, LE, K, INV>(sm), st.phase);
-    if constexpr (!INV) {
+    if constexpr (!INV && K == 2) {
+      // stage 1 (m = L/2) on x_j and x_{j+Q}: CTA 0 keeps the sums (Algorithm 3 lines 1-2), CTA 1
+      // the twiddled differences (lines 3-5, W = zeta_1^j).  The CTA-uniform choice is made outside
+      // the element loops so the loads (data and twiddles) are scheduled ahead of their use.
+      if (rank == 0) {
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; ++h) {
+            const int j = h * D + c[q];
+            v[q * S + h] = csub<W>(xb[j] + xb[j + Q], m.p2);
+          }
+      } else {
+        const int off = stage_off(LOGL, 1);
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; ++h) {
+            const int j = h * D + c[q];
+            W w, wp;
+            ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
+            v[q * S + h] = shoup_mul<W, PLO1>(xb[j] - xb[j + Q] + m.p2, w, wp, m);
+          }
+      }
+      // every CTA has read x_b: in-place stores below are safe.  (Measured: the relaxed
+      // cluster_sync_war() here makes the forward 15-35% slower, so the full barrier stays.)
+      cluster.sync();
+    } else if constexpr (!INV) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
