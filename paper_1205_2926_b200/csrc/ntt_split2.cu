@@ -235,10 +235,39 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
         for (int h = 0; h < S; ++h) sm[sswz<W>(h * D + c[q])] = v[q * S + h];
       cluster.sync();
+      constexpr int PER_CTA = Q / K;
+      if constexpr (K == 2) {
+        // stage 1 across the pair: this CTA finishes j in [rank Q/2, (rank+1) Q/2); its own block
+        // by LDS, the other's through DSMEM.  Groups of U positions with every load issued first,
+        // so the ~200-cycle DSMEM latency overlaps (it was the epilogue's main stall).
+        constexpr int IT = PER_CTA / Sh::T, U = IT >= 4 ? 4 : IT;
+        const W* other = cluster.map_shared_rank(sm, rank ^ 1);
+        const int off = stage_off(LOGL, 1);
+#pragma unroll 1
+        for (int j0 = 0; j0 < IT; j0 += U) {
+          W u0[U], u1[U], w[U], wp[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = rank * PER_CTA + t + Sh::T * (j0 + u);
+            const W mine = sm[sswz<W>(j)], theirs = other[sswz<W>(j)];
+            u0[u] = rank == 0 ? mine : theirs;  // x_j sits in CTA 0, x_{j+Q} in CTA 1
+            u1[u] = rank == 0 ? theirs : mine;
+            ldtw<W>(tw_full, (uint32_t)(off + j), w[u], wp[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = rank * PER_CTA + t + Sh::T * (j0 + u);
+            bfly_alg4<W, PLO1>(u0[u], u1[u], w[u], wp[u], m);
+            xb[j] = norm4<W>(u0[u], m.p, m.p2);
+            xb[j + Q] = norm4<W>(u1[u], m.p, m.p2);
+          }
+        }
+        cluster_sync_war();  // the other CTA is done reading this CTA's shared memory
+        return;
+      }
       const W* part[K];
 #pragma unroll
       for (int tt = 0; tt < K; ++tt) part[tt] = cluster.map_shared_rank(sm, tt);  // values at j + tt*Q
-      constexpr int PER_CTA = Q / K;
 #pragma unroll 2
       for (int jj = 0; jj < PER_CTA / Sh::T; ++jj) {
         const int j = rank * PER_CTA + t + Sh::T * jj;
