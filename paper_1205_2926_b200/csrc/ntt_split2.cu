@@ -240,7 +240,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         // stage 1 across the pair: this CTA finishes j in [rank Q/2, (rank+1) Q/2); its own block
         // by LDS, the other's through DSMEM.  Groups of U positions with every load issued first,
         // so the ~200-cycle DSMEM latency overlaps (it was the epilogue's main stall).
-        constexpr int IT = PER_CTA / Sh::T, U = IT >= 4 ? 4 : IT;
+        constexpr int UU = sizeof(W) == 4 ? 8 : 4, IT = PER_CTA / Sh::T, U = IT >= UU ? UU : IT;
         const W* other = cluster.map_shared_rank(sm, rank ^ 1);
         const int off = stage_off(LOGL, 1);
 #pragma unroll 1
