@@ -189,6 +189,16 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // this CTA's block of the bit-reversed input (contiguous runs, from shared memory);
       // PW: c = a b L^{-1} with b read from global memory 16 bytes at a time
       constexpr int PER = 16 / (int)sizeof(W);
+      if constexpr (PW) {  // every b load in flight first (into v itself), then combine with a
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; h += PER) {
+            const size_t off = (size_t)rank * Q + blk[q] * S + h;
+            unpack16<W>(__ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const W*>(pw.b) + boff + off)),
+                        v + q * S + h);
+          }
+      }
 #pragma unroll
       for (int q = 0; q < G; ++q) {
 #pragma unroll
@@ -196,12 +206,9 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           W av[PER];
           unpack16<W>(lds128(sm + tswz<W>(blk[q] * S + h)), av);
           if constexpr (PW) {
-            W bv[PER];
-            const size_t off = (size_t)rank * Q + blk[q] * S + h;
-            unpack16<W>(__ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const W*>(pw.b) + boff + off)), bv);
 #pragma unroll
             for (int e = 0; e < PER; ++e) {
-              W prod = mont_redc_mul<W>(av[e], bv[e], (W)pw.J, m.p);
+              W prod = mont_redc_mul<W>(av[e], v[q * S + h + e], (W)pw.J, m.p);
               v[q * S + h + e] = shoup_mul<W>(prod, (W)pw.K, (W)pw.Kp, m.p);
             }
           } else {
