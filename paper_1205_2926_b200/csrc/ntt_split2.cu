@@ -98,7 +98,7 @@ __device__ __forceinline__ void split_issue_own(const CUtensorMap* map, size_t b
 struct SplitStage {
   const CUtensorMap* map;
   uint32_t phase;
-  size_t next_b, batch;
+  size_t b, next_b, batch;
 };
 
 
@@ -232,8 +232,25 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     if constexpr (!INV) {
 #pragma unroll
       for (int i = 0; i < Sh::E; ++i) v[i] = norm2<W>(v[i], m.p);
+      // out through shared memory in the TMA 128-byte-swizzled layout and one bulk tensor store
+      // of the block: per-thread strided 16-byte global stores congested the LSU (lg_throttle, and
+      // long-scoreboard waits on the stores' source registers)
+      static_assert(D == 1, "the forward's last round holds contiguous runs");
+      constexpr int PER = 16 / (int)sizeof(W);
+      __syncthreads();  // every thread has read its last-round inputs from sm
 #pragma unroll
-      for (int q = 0; q < G; ++q) store_run<W, S>(xb + (size_t)rank * Q + blk[q] * S, v + q * S);
+      for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int h = 0; h < S; h += PER) sts128(sm + tswz<W>(blk[q] * S + h), pack16<W>(v + q * S + h));
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        constexpr int ROWS = Q * (int)sizeof(W) / 128, BOX = ROWS < 256 ? ROWS : 256;
+        const int row0 = (int)((st.b * K + (size_t)rank) * (size_t)ROWS);
+#pragma unroll
+        for (int bx = 0; bx < ROWS / BOX; ++bx) tma_store_2d(st.map, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
+        bulk_commit();
+      }
     } else {
       // stages s..1 across the cluster through DSMEM (Algorithm 4)
       __syncthreads();
@@ -300,6 +317,10 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       cluster_sync_war();  // the other CTAs are done reading this CTA's shared memory
     }
   } else {
+    // forward: the previous transform's bulk store must have read the buffer before it is reused
+    if constexpr (!INV) {
+      if (threadIdx.x == 0) bulk_wait_read0();
+    }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < G; ++q)
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
   const int rank = (int)cluster.block_rank();
   const int t = threadIdx.x;
   const Mod<W> m = make_mod<W>(p);
-  SplitStage st{&tmap, 0u, 0, batch};
+  SplitStage st{&tmap, 0u, 0, 0, batch};
   if constexpr (SplitStaging<W, LOGQ, LE, K, INV>::ON) {
     if (threadIdx.x == 0) {
       mbar_init(split_bar<W, LOGQ, LE, K, INV>(sm), 1);
@@ -346,6 +367,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
   for (uint32_t it = 0; b < batch; b += groups, ++it) {
     const size_t boff = b * (size_t)K * Sh::Q;
     st.phase = it & 1;
+    st.b = b;
     st.next_b = b + groups;
     constexpr int r0 = INV ? Sh::R - 1 : 0;
     split_round<W, LOGQ, LE, K, INV, PLO1, PW, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster, st);
@@ -357,6 +379,9 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
         split_issue_own<W, LOGQ, LE, K, INV>(st.map, st.next_b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
     }
     __syncthreads();
+  }
+  if constexpr (!INV) {
+    if (threadIdx.x == 0) bulk_wait0();  // shared memory must outlive the last bulk store
   }
 }
 
