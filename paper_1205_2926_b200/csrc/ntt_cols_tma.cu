@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
       bulk_commit();
     }
   }
-  if (threadIdx.x == 0) bulk_wait0();  // smem must outlive the last bulk store
+  // the last bulk store must have read shared memory before the CTA exits (its global writes
+  // complete with the grid, as CUTLASS's TMA epilogues rely on)
+  if (threadIdx.x == 0) bulk_wait_read0();
 }
 
 // ----------------------------------------------------------------- host side

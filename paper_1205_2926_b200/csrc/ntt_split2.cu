@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     __syncthreads();
   }
   if constexpr (!INV) {
-    if (threadIdx.x == 0) bulk_wait0();  // shared memory must outlive the last bulk store
+    if (threadIdx.x == 0) bulk_wait_read0();  // the last bulk store has read shared memory
   }
 }
 
