@@ -20,6 +20,9 @@
  *   later call or a stream synchronisation.  No C++ exception crosses the ABI.
  * - Input ranges are preconditions (not checked in the hot path): forward
  *   needs x < 2p (Alg. 3 input), inverse needs x < 4p (Alg. 4).
+ *   ntt_set_range_checks(1) turns on a checking mode in which ntt_forward /
+ *   ntt_inverse first scan their input on the stream, synchronise, and return
+ *   NTT_ERR_RANGE (data untouched) if any word is out of range.
  * - Outputs are always normalised to [0,p) ("normalise the final NTT
  *   output"); bit-exactness is defined on these canonical values.
  * - A plan is immutable after creation and may be shared by threads and
@@ -47,7 +50,8 @@ typedef enum {
   NTT_ERR_WORD = -5,        /* log2_beta not in {32, 64} */
   NTT_ERR_CUDA = -6,        /* a CUDA runtime error (see ntt_last_cuda_error) */
   NTT_ERR_NOMEM = -7,       /* device or host allocation failed at plan creation */
-  NTT_ERR_UNSUPPORTED = -8  /* valid request this build does not implement */
+  NTT_ERR_UNSUPPORTED = -8, /* valid request this build does not implement */
+  NTT_ERR_RANGE = -9        /* range-checking mode: an input word is >= 2p (forward) / 4p (inverse) */
 } ntt_status;
 
 /* ntt_pointwise_mul flags */
@@ -226,6 +230,13 @@ ntt_status ntt_debug_butterfly(ntt_plan_t plan, int alg, const void* W, const vo
  * sink: device buffer of >= 16 bytes (defeats dead-code elimination). */
 ntt_status ntt_calibrate_butterfly(unsigned log2_beta, uint64_t p, uint64_t W, uint64_t Wp, unsigned iters,
                                    void* sink, uint64_t* n_butterflies, ntt_stream_t stream);
+
+/* Range-checking mode (process-wide, default off): when on, ntt_forward / ntt_inverse
+ * verify their input against the Algorithm 3 / 4 preconditions (x < 2p, x < 4p; P:114,
+ * P:146) with a device scan and a stream synchronisation before transforming, and return
+ * NTT_ERR_RANGE without modifying x on a violation.  A debugging aid: it costs a full
+ * read of the data and a host round trip per call.  Returns the previous setting. */
+unsigned ntt_set_range_checks(unsigned on);
 
 /* Number of kernel launches the last transform entry point on this thread issued. */
 unsigned ntt_last_launch_count(void);

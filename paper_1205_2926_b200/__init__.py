@@ -19,7 +19,7 @@ NTT_OP_INVERSE = 2
 
 _STATUS = {
     0: "NTT_OK", -1: "NTT_ERR_ARG", -2: "NTT_ERR_MODULUS", -3: "NTT_ERR_ROOT", -4: "NTT_ERR_LENGTH",
-    -5: "NTT_ERR_WORD", -6: "NTT_ERR_CUDA", -7: "NTT_ERR_NOMEM", -8: "NTT_ERR_UNSUPPORTED",
+    -5: "NTT_ERR_WORD", -6: "NTT_ERR_CUDA", -7: "NTT_ERR_NOMEM", -8: "NTT_ERR_UNSUPPORTED", -9: "NTT_ERR_RANGE",
 }
 
 
@@ -79,6 +79,8 @@ def _load() -> ctypes.CDLL:
     lib.ntt_status_str.restype = ctypes.c_char_p
     lib.ntt_last_cuda_error.restype = ctypes.c_char_p
     lib.ntt_last_launch_count.restype = uint
+    lib.ntt_set_range_checks.argtypes = [uint]
+    lib.ntt_set_range_checks.restype = uint
     lib.ntt_abi_version.restype = uint
     return lib
 
@@ -90,7 +92,7 @@ EXPORTED = (
     "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
     "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p",
     "ntt_fourstep_rows_inv_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
-    "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
+    "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_set_range_checks", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
 )
 
 
@@ -122,6 +124,11 @@ def _stream(stream) -> int:
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def set_range_checks(on: bool) -> bool:
+    """ntt_set_range_checks: debugging mode validating transform inputs (returns the previous setting)."""
+    return bool(_lib.ntt_set_range_checks(1 if on else 0))
 
 
 def last_launch_count() -> int:

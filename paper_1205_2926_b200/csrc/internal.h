@@ -96,6 +96,7 @@ cudaError_t launch_crt3(uint64_t* out, const uint32_t* r0, const uint32_t* r1, c
 cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, size_t n, uint64_t p, uint64_t J,
                              uint64_t K, uint64_t Kp, cudaStream_t s);
 cudaError_t launch_normalize(int wbytes, void* x, size_t n, uint64_t p, int from4p, cudaStream_t s);
+cudaError_t launch_check_range(int wbytes, const void* x, size_t n, uint64_t bound, unsigned* flag, cudaStream_t s);
 cudaError_t launch_synth(int wbytes, void* x, size_t count, uint64_t seed, uint64_t tensor_id, uint64_t start,
                          uint64_t bound, unsigned bits, cudaStream_t s);
 cudaError_t launch_calib(int wbytes, uint64_t p, uint64_t w, uint64_t wp, unsigned iters, void* sink,

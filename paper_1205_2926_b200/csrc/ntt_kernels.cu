@@ -589,6 +589,25 @@ cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, 
   return cudaGetLastError();
 }
 
+// Range-checking mode: flag[0] |= 1 if any word is >= bound.
+template <class W>
+__global__ void k_check_range(const W* __restrict__ x, size_t n, W bound, unsigned* flag) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) bad |= x[i] >= bound;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+cudaError_t launch_check_range(int wbytes, const void* x, size_t n, uint64_t bound, unsigned* flag, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const int th = 256;
+  if (wbytes == 8)
+    k_check_range<uint64_t><<<elementwise_grid(n, th), th, 0, s>>>((const uint64_t*)x, n, bound, flag);
+  else
+    k_check_range<uint32_t><<<elementwise_grid(n, th), th, 0, s>>>((const uint32_t*)x, n, (uint32_t)bound, flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_normalize(int wbytes, void* x, size_t n, uint64_t p, int from4p, cudaStream_t s) {
   if (!n) return cudaSuccess;
   const int th = 256;

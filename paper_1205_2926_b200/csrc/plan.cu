@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -312,6 +313,7 @@ const char* ntt_status_str(ntt_status s) {
     case NTT_ERR_CUDA: return "CUDA error";
     case NTT_ERR_NOMEM: return "out of memory";
     case NTT_ERR_UNSUPPORTED: return "unsupported";
+    case NTT_ERR_RANGE: return "input word out of the butterfly's accepted range";
   }
   return "unknown status";
 }
@@ -467,6 +469,22 @@ static cudaError_t launch_cols_any(int wbytes, int logn, bool inverse, void* x, 
   return nttb::launch_cols(wbytes, logn, inverse, x, prm, t, p, s);
 }
 
+static std::atomic<unsigned> g_range_checks{0};
+
+// Range-checking mode: scan x for words >= bound; NTT_ERR_RANGE on a violation.
+static ntt_status check_range(ntt_plan_t pl, const void* x, size_t n, uint64_t bound, cudaStream_t s) {
+  unsigned* flag = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&flag, sizeof(unsigned), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(unsigned), s);
+  if (e == cudaSuccess) e = nttb::launch_check_range((int)pl->wbytes, x, n, bound, flag, s);
+  unsigned h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (flag) cudaFreeAsync(flag, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return h ? NTT_ERR_RANGE : NTT_OK;
+}
+
 static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
   t_launches = 0;
   if (!pl || (!x && batch) || (x && !aligned16(x))) return NTT_ERR_ARG;
@@ -475,6 +493,12 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
   if (batch > (SIZE_MAX / pl->wbytes) / L) return NTT_ERR_ARG;
   DeviceGuard g(pl->device);
   if (!g.ok) return cuda_fail(cudaGetLastError());
+  if (g_range_checks.load(std::memory_order_relaxed)) {
+    // Alg. 3 takes [0,2p) (Alg. 2 plans canonical [0,p)), Alg. 4 [0,4p)
+    const uint64_t bound = inverse ? 4 * pl->p : (pl->bfly == NTT_BFLY_ALG2 ? pl->p : 2 * pl->p);
+    ntt_status st = check_range(pl, x, batch * L, bound, s);
+    if (st != NTT_OK) return st;
+  }
   cudaError_t e = cudaSuccess;
   const unsigned np = (unsigned)pl->passes.size();
   if (pl->ell == 0) {  // identity; only the normalisation remains
@@ -628,6 +652,8 @@ ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, vo
   t_launches = launches;
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
+
+unsigned ntt_set_range_checks(unsigned on) { return g_range_checks.exchange(on ? 1u : 0u); }
 
 ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream) {
   return run_transform(plan, x, batch, (cudaStream_t)stream, false);

@@ -34,7 +34,7 @@ def test_header_symbols_exported(ntt):
 def test_abi_version_and_status_strings(ntt):
     lib = ntt.lib()
     assert lib.ntt_abi_version() == 1
-    for s in range(-8, 1):
+    for s in range(-9, 1):
         assert lib.ntt_status_str(s)
 
 

@@ -398,3 +398,30 @@ def test_u64_three_pass_lengths(ntt, ell):
     ih = x.cpu().numpy()
     idx = rng.integers(0, L, 1 << 17)
     assert all(int(ih[i]) == int(xh[i]) * L % p for i in idx)
+
+
+def test_range_checking_mode(ntt):
+    """ntt_set_range_checks: inputs outside Algorithm 3's [0,2p) / Algorithm 4's [0,4p)
+    are refused with NTT_ERR_RANGE and left untouched; the tops of the ranges are accepted."""
+    p, ell = P62, 12
+    plan = ntt.Plan(p, root(p, 1 << ell), ell, 64)
+    prev = ntt.set_range_checks(True)
+    try:
+        x = np.full((2, 1 << ell), 2 * p - 1, dtype=np.uint64)
+        d = to_dev(x, 64)
+        plan.forward(d)  # 2p - 1 is legal
+        x[1, 77] = 2 * p
+        d = to_dev(x, 64)
+        with pytest.raises(ntt.NttError) as ei:
+            plan.forward(d)
+        assert ei.value.status == -9
+        assert np.array_equal(to_host(d), x)  # untouched
+        y = np.full((1, 1 << ell), 4 * p - 1, dtype=np.uint64)
+        dy = to_dev(y, 64)
+        plan.inverse(dy)  # 4p - 1 is legal for Algorithm 4
+        y[0, 5] = 4 * p
+        dy = to_dev(y, 64)
+        with pytest.raises(ntt.NttError):
+            plan.inverse(dy)
+    finally:
+        ntt.set_range_checks(prev)
