@@ -425,3 +425,54 @@ def test_range_checking_mode(ntt):
             plan.inverse(dy)
     finally:
         ntt.set_range_checks(prev)
+
+
+@pytest.mark.parametrize("bits,p,ell,batch,buf_transforms", [
+    (64, P62, 12, 4096, 2048), (64, P62, 12, 37, 1), (32, P30, 10, 1000, 7), (64, P62, 18, 3, 1), (32, RNS[0], 16, 5, 2),
+])
+def test_execute_host_pipeline(ntt, bits, p, ell, batch, buf_transforms):
+    """ntt_execute_host (host buffers in and out, H2D / transforms / D2H pipelined over a device ring):
+    forward, inverse and both, bit-exact with the device-resident calls, for ragged chunkings down to
+    a one-transform device buffer."""
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(batch * L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(2), 11, bound=p)
+    h_in = x.cpu().pin_memory()
+    dbuf = torch.empty(buf_transforms * L, dtype=dt, device="cuda")
+    ref_f = x.clone()
+    plan.forward(ref_f)
+    ref_fi = ref_f.clone()
+    plan.inverse(ref_fi)
+    ref_i = x.clone()
+    plan.inverse(ref_i)
+    for ops, ref in ((ntt.NTT_OP_FORWARD, ref_f), (ntt.NTT_OP_INVERSE, ref_i),
+                     (ntt.NTT_OP_FORWARD | ntt.NTT_OP_INVERSE, ref_fi)):
+        h_out = torch.empty_like(h_in).pin_memory()
+        plan.execute_host(ops, h_in, h_out, dbuf)
+        torch.cuda.synchronize()
+        assert torch.equal(h_out.view(torch.int64 if bits == 64 else torch.int32),
+                           ref.cpu().view(torch.int64 if bits == 64 else torch.int32)), ops
+
+
+@pytest.mark.parametrize("bits,p,ell,batch", [(64, P62, 12, 9), (64, P62, 17, 2), (32, P30, 11, 5)])
+def test_cyclic_convolution_other_shapes(ntt, bits, p, ell, batch):
+    """ntt_cyclic_convolve beyond C3's shape (single-pass u64, multi-pass with separate pointwise): each
+    pair against the oracle's per-coefficient definition on sampled k and the oracle NTT route."""
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    rng = np.random.default_rng(ell + bits)
+    a = rand_residues(rng, p, (batch, L))
+    b = rand_residues(rng, p, (batch, L))
+    da, db = to_dev(a, bits), to_dev(b, bits)
+    plan.cyclic_convolve(da, db)
+    got = to_host(da)
+    for i in (0, batch - 1):
+        ref = oracle.ntt_inverse(p, w, oracle.pointwise(p, oracle.ntt_forward(p, w, a[i]), oracle.ntt_forward(p, w, b[i]),
+                                                        scale_L=L))
+        assert np.array_equal(got[i], ref)
+        for k in (0, 1, L // 2, L - 1):
+            assert int(got[i, k]) == oracle.cyclic_conv_coeff(p, a[i], b[i], k)
