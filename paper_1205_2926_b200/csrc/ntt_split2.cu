@@ -260,7 +260,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         for (int h = 0; h < S; ++h) sm[sswz<W>(h * D + c[q])] = v[q * S + h];
       cluster.sync();
       constexpr int PER_CTA = Q / K;
-      if constexpr (K == 2) {
+      if constexpr (K == 2) {  // (K = 4: the general loop below)
         // stage 1 across the pair: this CTA finishes j in [rank Q/2, (rank+1) Q/2); its own block
         // by LDS, the other's through DSMEM.  Groups of U positions with every load issued first,
         // so the ~200-cycle DSMEM latency overlaps (it was the epilogue's main stall).
@@ -287,34 +287,34 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           }
         }
         cluster_sync_war();  // the other CTA is done reading this CTA's shared memory
-        return;
-      }
-      const W* part[K];
+      } else {
+        const W* part[K];
 #pragma unroll
-      for (int tt = 0; tt < K; ++tt) part[tt] = cluster.map_shared_rank(sm, tt);  // values at j + tt*Q
+        for (int tt = 0; tt < K; ++tt) part[tt] = cluster.map_shared_rank(sm, tt);  // values at j + tt*Q
 #pragma unroll 2
-      for (int jj = 0; jj < PER_CTA / Sh::T; ++jj) {
-        const int j = rank * PER_CTA + t + Sh::T * jj;
-        W u[K];
+        for (int jj = 0; jj < PER_CTA / Sh::T; ++jj) {
+          const int j = rank * PER_CTA + t + Sh::T * jj;
+          W u[K];
 #pragma unroll
-        for (int tt = 0; tt < K; ++tt) u[tt] = part[tt][sswz<W>(j)];
+          for (int tt = 0; tt < K; ++tt) u[tt] = part[tt][sswz<W>(j)];
 #pragma unroll
-        for (int i = SS; i >= 1; --i) {
-          const int half = K >> i;  // pairs (tt, tt + half) inside blocks of 2*half
-          const int off = stage_off(LOGL, i);
+          for (int i = SS; i >= 1; --i) {
+            const int half = K >> i;  // pairs (tt, tt + half) inside blocks of 2*half
+            const int off = stage_off(LOGL, i);
 #pragma unroll
-          for (int bb = 0; bb < K; bb += 2 * half)
+            for (int bb = 0; bb < K; bb += 2 * half)
 #pragma unroll
-            for (int tt = 0; tt < half; ++tt) {
-              W w, wp;
-              ldtw<W>(tw_full, (uint32_t)(off + j + tt * Q), w, wp);
-              bfly_alg4<W, PLO1>(u[bb + tt], u[bb + tt + half], w, wp, m);
-            }
+              for (int tt = 0; tt < half; ++tt) {
+                W w, wp;
+                ldtw<W>(tw_full, (uint32_t)(off + j + tt * Q), w, wp);
+                bfly_alg4<W, PLO1>(u[bb + tt], u[bb + tt + half], w, wp, m);
+              }
+          }
+#pragma unroll
+          for (int tt = 0; tt < K; ++tt) xb[j + tt * Q] = norm4<W>(u[tt], m.p, m.p2);
         }
-#pragma unroll
-        for (int tt = 0; tt < K; ++tt) xb[j + tt * Q] = norm4<W>(u[tt], m.p, m.p2);
+        cluster_sync_war();  // the other CTAs are done reading this CTA's shared memory
       }
-      cluster_sync_war();  // the other CTAs are done reading this CTA's shared memory
     }
   } else {
     // forward: the previous transform's bulk store must have read the buffer before it is reused

@@ -801,8 +801,6 @@ ntt_status ntt_fourstep_rows(ntt_plan_t pl, unsigned ell1, const void* recv, voi
   while ((1u << lw) < world) ++lw;
   if (lw > ell1 || lw > ell2) return NTT_ERR_ARG;
   DeviceGuard g(pl->device);
-  const uint64_t L = (uint64_t)1 << pl->ell;
-  const uint64_t N2 = (uint64_t)1 << ell2;
   void* subf = nullptr;
   ntt_status st = sub_table(pl, ell2, &subf);
   if (st != NTT_OK) return st;
