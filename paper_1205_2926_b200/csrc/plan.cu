@@ -135,14 +135,14 @@ struct ntt_plan_s {
   void* tw_fwd = nullptr;  // single pass: omega^e, e < L/2
   void* tw_inv = nullptr;  // single pass: omega^{-e}
   std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables
-  void* fa = nullptr;                   // four-step table (direct when H == 0)
-  void* fb = nullptr;
-  unsigned H = 0;
   std::vector<void*> owned;
   // lazily built tables for the distributed four-step entry points (guarded by mu)
   std::mutex mu;
   std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e table
   std::map<unsigned, void*> extra_sub_inv;  // log2 N -> omega_N^{-e} table
+  // four-step twiddle tables per block level: log2 B -> (table A, table B, H) for omega_B^e, e < B
+  struct FsTables { void* fa; void* fb; unsigned H; };
+  std::map<unsigned, FsTables> fs_level;
   // host-buffer executor (ntt_execute_host): pipeline streams and events
   static constexpr int kRing = 8;           // max device buffers in the host pipeline's ring
   static constexpr int kDefaultRing = 4;
@@ -265,35 +265,37 @@ ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out, bool inverse = f
   return NTT_OK;
 }
 
-// Four-step twiddles omega_L^e, e < L: direct table for ell <= 16, else factored
-// omega^e = omega^{(e >> H) << H} * omega^{e & (2^H - 1)} (two Shoup multiplies).
-ntt_status build_fourstep_tables(ntt_plan_s* pl) {
-  const uint64_t L = (uint64_t)1 << pl->ell;
+// Four-step twiddles of a column pass whose blocks hold B = 2^lb words: omega_B^e, e < B (omega_B =
+// omega^{L/B}), so a pass indexes its own tables with e = c rev(r) instead of e << log2(L/B) into
+// one L-level table (whose entries a warp's neighbouring columns then hit far apart: C5's second
+// column pass).  Direct table for lb <= 16, else factored omega_B^e = omega_B^{(e >> H) << H} *
+// omega_B^{e & (2^H - 1)} (two Shoup multiplies) with H = min(ceil(lb / 2), 10): the low factor
+// (indexed by e mod 2^H, scattered across a warp) stays in L1, the high one (indexed by e >> H,
+// nearly uniform across neighbouring columns) in L2.  Measured C5: H = 14 6.37 ms, H = 10 6.06 ms.
+ntt_status fourstep_level_tables(ntt_plan_s* pl, unsigned lb, ntt_plan_s::FsTables* out) {
+  std::lock_guard<std::mutex> lk(pl->mu);
+  auto it = pl->fs_level.find(lb);
+  if (it != pl->fs_level.end()) { *out = it->second; return NTT_OK; }
+  const uint64_t B = (uint64_t)1 << lb;
+  const uint64_t root = powmod(pl->omega, ((uint64_t)1 << pl->ell) >> lb, pl->p);
+  ntt_plan_s::FsTables t{nullptr, nullptr, 0};
   ntt_status st;
-  if (pl->ell <= 16) {
-    pl->H = 0;
-    st = upload(pl, make_table(pl->p, pl->omega, L, pl->bits), &pl->fa);
-    pl->fb = pl->fa;
+  if (lb <= 16) {
+    st = upload(pl, make_table(pl->p, root, B, pl->bits), &t.fa);
+    t.fb = t.fa;
   } else {
-    // split of the factored table: the low factor (2^H entries, indexed by e mod 2^H, scattered
-    // across a warp) small enough to stay in L1, the high factor (2^{ell-H} entries, indexed by
-    // e >> H, nearly uniform across a warp's neighbouring columns) in L2.  Measured C5 (ell = 28):
-    // H = 14 6.37 ms, H = 10 6.06 ms; C4 (ell = 24): flat for H = 8..12.
-    pl->H = std::min((pl->ell + 1) / 2, 10u);
+    t.H = std::min((lb + 1) / 2, 10u);
     if (const char* e = getenv("NTT_FOURSTEP_H")) {  // experiment hook
       const unsigned h = (unsigned)atoi(e);
-      if (h >= 1 && h < pl->ell) pl->H = h;
+      if (h >= 1 && h < lb) t.H = h;
     }
-    st = upload(pl, make_table(pl->p, powmod(pl->omega, (uint64_t)1 << pl->H, pl->p), L >> pl->H, pl->bits), &pl->fa);
-    if (st == NTT_OK) st = upload(pl, make_table(pl->p, pl->omega, (uint64_t)1 << pl->H, pl->bits), &pl->fb);
+    st = upload(pl, make_table(pl->p, powmod(root, (uint64_t)1 << t.H, pl->p), B >> t.H, pl->bits), &t.fa);
+    if (st == NTT_OK) st = upload(pl, make_table(pl->p, root, (uint64_t)1 << t.H, pl->bits), &t.fb);
   }
-  return st;
-}
-
-ntt_status ensure_fourstep_tables(ntt_plan_s* pl) {
-  std::lock_guard<std::mutex> lk(pl->mu);
-  if (pl->fa) return NTT_OK;
-  return build_fourstep_tables(pl);
+  if (st != NTT_OK) return st;
+  pl->fs_level[lb] = t;
+  *out = t;
+  return NTT_OK;
 }
 
 }  // namespace
@@ -393,8 +395,12 @@ ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsig
       pl->sub_fwd.push_back(f);
       pl->sub_inv.push_back(i);
     }
-    st = build_fourstep_tables(pl);
-    if (st != NTT_OK) { free_plan(pl); return st; }
+    unsigned outer = 0;
+    for (size_t j = 0; j + 1 < pl->passes.size(); ++j) {
+      ntt_plan_s::FsTables t;
+      if ((st = fourstep_level_tables(pl, ell - outer, &t)) != NTT_OK) { free_plan(pl); return st; }
+      outer += pl->passes[j];
+    }
   }
   *out = pl;
   return NTT_OK;
@@ -530,17 +536,29 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     prm.log_S = logS;
     prm.log_colgroups = logS - logC;
     prm.n_tiles = ((uint64_t)batch << outer) << prm.log_colgroups;
-    prm.log_tw_mul = outer;
-    prm.ell = pl->ell;
-    prm.H = pl->H;
+    // per-level tables: exponent e = c rev(r) of omega_B, B = 2^logB (log_tw_mul = 0, ell = logB)
+    prm.log_tw_mul = 0;
+    prm.ell = logB;
     prm.twiddle = 1;
     prm.normalize = normalize ? 1 : 0;
     return prm;
   };
+  auto level_tables = [&](unsigned j, nttb::ColsParams& prm, const void** fa, const void** fb) {
+    ntt_plan_s::FsTables t{};
+    const ntt_status st = fourstep_level_tables(pl, prm.ell, &t);  // built at plan creation: a cache hit
+    prm.H = t.H;
+    *fa = t.fa;
+    *fb = t.fb;
+    (void)j;
+    return st;
+  };
   if (!inverse) {
     for (unsigned j = 0; j + 1 < np && e == cudaSuccess; ++j) {
-      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
-      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], false, x, cols_params(j, false), t, pl->p, s);
+      nttb::ColsParams prm = cols_params(j, false);
+      const void *fa = nullptr, *fb = nullptr;
+      if (ntt_status st = level_tables(j, prm, &fa, &fb); st != NTT_OK) return st;
+      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], fa, fb};
+      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], false, x, prm, t, pl->p, s);
       ++t_launches;
     }
     if (e == cudaSuccess) {
@@ -553,8 +571,11 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     e = launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], true, false, x, rows, pl->sub_inv[np - 1], pl->p, s);
     ++t_launches;
     for (int j = (int)np - 2; j >= 0 && e == cudaSuccess; --j) {
-      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], pl->fa, pl->fb};
-      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], true, x, cols_params((unsigned)j, j == 0), t, pl->p, s);
+      nttb::ColsParams prm = cols_params((unsigned)j, j == 0);
+      const void *fa = nullptr, *fb = nullptr;
+      if (ntt_status st = level_tables((unsigned)j, prm, &fa, &fb); st != NTT_OK) return st;
+      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], fa, fb};
+      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], true, x, prm, t, pl->p, s);
       ++t_launches;
     }
   }
@@ -720,11 +741,8 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
   unsigned logC = 0;
   while ((1u << logC) < C) ++logC;
   DeviceGuard g(pl->device);
-  {
-    ntt_status st = ensure_fourstep_tables(pl);  // before reading pl->H
-    if (st != NTT_OK) return st;
-  }
   std::vector<nttb::ColsParams> prms(nc);
+  std::vector<ntt_plan_s::FsTables> tabs(nc);
   unsigned outer = 0;
   for (unsigned j = 0; j < nc; ++j) {
     const unsigned logN = cp[j];
@@ -735,9 +753,11 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
     prm.log_S = logS;
     prm.log_colgroups = logS - logC;
     prm.n_tiles = ((uint64_t)1 << outer) << prm.log_colgroups;
-    prm.log_tw_mul = outer;
-    prm.ell = pl->ell;
-    prm.H = pl->H;
+    // per-level tables of omega_B, B = 2^(ell - outer): e = c rev(r) (c: global column of the block)
+    prm.log_tw_mul = 0;
+    prm.ell = pl->ell - outer;
+    if (ntt_status st = fourstep_level_tables(pl, prm.ell, &tabs[j]); st != NTT_OK) return st;
+    prm.H = tabs[j].H;
     prm.twiddle = 1;
     prm.normalize = (inverse && j == 0) ? 1 : 0;  // the inverse's last pass writes canonical values
     prm.shard = 1;
@@ -764,7 +784,7 @@ static ntt_status fourstep_cols_impl(ntt_plan_t pl, unsigned ell1, void* x, unsi
     void* sub = nullptr;
     ntt_status st = sub_table(pl, cp[j], &sub, inverse);
     if (st != NTT_OK) return st;
-    nttb::DevTables t{sub, sub, pl->fa, pl->fb};
+    nttb::DevTables t{sub, sub, tabs[j].fa, tabs[j].fb};
     e = prms[j].p2p ? nttb::launch_cols_tma(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream)
                     : launch_cols_any(pl->wbytes, (int)cp[j], inverse, x, prms[j], t, pl->p, (cudaStream_t)stream);
     ++t_launches;
