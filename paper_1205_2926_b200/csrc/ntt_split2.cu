@@ -4,12 +4,14 @@
 // Forward (Algorithm 1): after the first s = log2 K stages, the block of
 // positions [rQ, (r+1)Q) is an independent Q-point transform with root omega^K
 // (stages s+1..ell), whose per-stage twiddle table is the full table's suffix from
-// offset L - Q.  CTA r evaluates only its path through stages 1..s straight from HBM:
-// for each j < Q it loads x_{j + tQ} (t < K) and, at stage i, keeps the sum
-// (Algorithm 3 lines 1-2) or the twiddled difference (lines 3-5, W = zeta_i^{j + tQ})
-// as bit (s - i) of r says.  (Stage 1 is evaluated by two CTAs when K = 4: +1/ell
-// work, no data exchange.)  A cluster barrier after the loads orders every CTA's
-// reads before the in-place stores; output block r = Alg. 1's positions [rQ, (r+1)Q).
+// offset L - Q.  CTA r evaluates only its path through stages 1..s: for each j < Q it
+// reads x_{j + tQ} (t < K) and, at stage i, keeps the sum (Algorithm 3 lines 1-2) or the
+// twiddled difference (lines 3-5, W = zeta_i^{j + tQ}) as bit (s - i) of r says.  (Stage 1
+// is evaluated by two CTAs when K = 4: +1/ell work, no data exchange.)  K = 2 brings both
+// blocks in by TMA, in chunks through shared memory, the first ones while the previous
+// transform computes (SplitFwd); K = 4 loads them from global memory.  A cluster barrier
+// orders every CTA's reads before the in-place stores (K = 2: arrive after stage 1, wait
+// before the last round's store); output block r = Alg. 1's positions [rQ, (r+1)Q).
 //
 // Inverse (Algorithm 1 run backwards): stages ell..s+1 are K independent
 // Q-point inverses (one per CTA); stages s..1 (Algorithm 4, W = zeta_i^{-k}) act on
@@ -102,6 +104,81 @@ struct SplitStage {
   size_t b, next_b, batch;
 };
 
+#ifndef NTT_SPLIT_NX
+#define NTT_SPLIT_NX 3
+#endif
+
+// Forward staging (K = 2): the first round's inputs x_{hD + t} and x_{Q + hD + t} (h < 32) come in
+// NCH chunks of HC h-rows of both blocks (2 x HC x D words; one TMA box of 128-byte rows per
+// block).  NX chunk slots sit after the Q-word buffer and are filled with the next transform's
+// first chunks while this one computes; the next 4 chunks land in the Q-word buffer itself once
+// the previous transform's bulk store has read it, the rest in the X slots once consumed.
+template <class W, int LOGQ, int LE> struct SplitFwd {
+  static constexpr int Q = 1 << LOGQ, S = 1 << Rounds<LOGQ, LE>::sr(0), D = Q / S;
+  static constexpr int NCH = 8, HC = S / NCH, NX = NTT_SPLIT_NX, NB = 4;
+  static constexpr uint32_t HALF = (uint32_t)(HC * D * sizeof(W)), CH = 2 * HALF;
+  static constexpr int BOXR = (int)(HALF / 128);  // rows of one block's part of a chunk
+  static constexpr uint32_t X_OFF = (uint32_t)(Q * sizeof(W)), BAR_OFF = X_OFF + NX * CH;
+  static constexpr size_t SMEM = BAR_OFF + NCH * 8;
+  static_assert(NB * CH == (uint32_t)(Q * sizeof(W)), "4 chunks fill the Q-word buffer");
+  static_assert(NX + NB < NCH && NCH - NX - NB <= NX, "late chunks reuse X slots");
+  static_assert(HALF % 1024 == 0 && BOXR <= 256, "swizzle period / TMA box");
+  __device__ static constexpr uint32_t slot(int k) {
+    return k < NX ? X_OFF + k * CH : (k < NX + NB ? (k - NX) * CH : X_OFF + (k - NX - NB) * CH);
+  }
+  // chunk k of transform b: two boxes (block 0 rows, block 1 rows) into its slot
+  __device__ static void issue(const CUtensorMap* map, size_t b, int k, uint32_t sbase) {
+    const uint32_t bar = sbase + BAR_OFF + 8 * k, dst = sbase + slot(k);
+    constexpr int ROWS_BLK = (int)(Q * sizeof(W) / 128);
+    mbar_expect_tx(bar, CH);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+      tma_load_2d(dst + hf * HALF, map, 0, (int)((b * 2 + hf) * (size_t)ROWS_BLK) + k * BOXR, bar);
+  }
+};
+
+// Stage 1 of the forward from the staged chunks: CTA 0 keeps sums, CTA 1 twiddled differences.
+template <class W, int LOGQ, int LE, int LOGL, bool PLO1, bool UPPER>
+__device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const TwPair<W>* __restrict__ tw_full,
+                                                 const Mod<W>& m, const SplitStage& st) {
+  using F = SplitFwd<W, LOGQ, LE>;
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(sm);
+  const uint32_t sbase = smem_u32(sm);
+  const int tsw = tswz<W>(t);  // (h - h0) D is a multiple of the swizzle period
+  const int off = stage_off(LOGL, 1);
+#pragma unroll
+  for (int k = 0; k < F::NCH; ++k) {
+    mbar_wait(sbase + F::BAR_OFF + 8 * k, st.phase);
+    const W* lo = reinterpret_cast<const W*>(base + F::slot(k));
+    const W* hi = reinterpret_cast<const W*>(base + F::slot(k) + F::HALF);
+#pragma unroll
+    for (int hh = 0; hh < F::HC; ++hh) {
+      const int h = k * F::HC + hh, j = h * F::D + t;
+      const W a = lo[hh * F::D + tsw], b = hi[hh * F::D + tsw];
+      if constexpr (!UPPER) {
+        v[h] = csub<W>(a + b, m.p2);
+      } else {
+        W w, wp;
+        ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
+        v[h] = shoup_mul<W, PLO1>(a - b + m.p2, w, wp, m);
+      }
+    }
+    if (k == F::NX - 1) {  // X slots consumed: the late chunks reuse them
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0)
+#pragma unroll
+        for (int kk = F::NX + F::NB; kk < F::NCH; ++kk) F::issue(st.map, st.b, kk, sbase);
+    }
+  }
+  // every chunk consumed: the X slots take the next transform's first chunks
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0 && st.next_b < st.batch)
+#pragma unroll
+    for (int kk = 0; kk < F::NX; ++kk) F::issue(st.map, st.next_b, kk, sbase);
+}
+
 
 template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW, int r>
 __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int t, int rank,
@@ -131,26 +208,9 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // stage 1 (m = L/2) on x_j and x_{j+Q}: CTA 0 keeps the sums (Algorithm 3 lines 1-2), CTA 1
       // the twiddled differences (lines 3-5, W = zeta_1^j).  The CTA-uniform choice is made outside
       // the element loops so the loads (data and twiddles) are scheduled ahead of their use.
-      if (rank == 0) {
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-#pragma unroll
-          for (int h = 0; h < S; ++h) {
-            const int j = h * D + c[q];
-            v[q * S + h] = csub<W>(xb[j] + xb[j + Q], m.p2);
-          }
-      } else {
-        const int off = stage_off(LOGL, 1);
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-#pragma unroll
-          for (int h = 0; h < S; ++h) {
-            const int j = h * D + c[q];
-            W w, wp;
-            ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
-            v[q * S + h] = shoup_mul<W, PLO1>(xb[j] - xb[j + Q] + m.p2, w, wp, m);
-          }
-      }
+      static_assert(G == 1 && S == SplitFwd<W, LOGQ, LE>::S, "first round: one column per thread");
+      if (rank == 0) split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, false>(v, sm, t, tw_full, m, st);
+      else split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, true>(v, sm, t, tw_full, m, st);
       // every CTA has read x_b (the loaded values are consumed, so a relaxed arrive orders them):
       // arrive here, wait only before the last round's in-place store.  Measured against a full
       // cluster.sync() at this point: u32 2^16 -7%, u64 2^15 -3% (the wait no longer stalls the
@@ -249,7 +309,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       __syncthreads();
       if constexpr (K == 2) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // partner read x_b
       if (threadIdx.x == 0) {
-        constexpr int ROWS = Q * (int)sizeof(W) / 128, BOX = ROWS < 256 ? ROWS : 256;
+        constexpr int ROWS = Q * (int)sizeof(W) / 128;
+        constexpr int BOX = (K == 2) ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256);
         const int row0 = (int)((st.b * K + (size_t)rank) * (size_t)ROWS);
 #pragma unroll
         for (int bx = 0; bx < ROWS / BOX; ++bx) tma_store_2d(st.map, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
@@ -364,15 +425,36 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     }
     __syncthreads();
   }
+  constexpr bool FWD_TMA = !INV && K == 2;
+  using F = SplitFwd<W, LOGQ, LE>;
   W v[Sh::E];
   const size_t groups = gridDim.x / K;
   size_t b = blockIdx.x / K;
+  if constexpr (FWD_TMA) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < F::NCH; ++k) mbar_init(smem_u32(sm) + F::BAR_OFF + 8 * k, 1);
+      fence_mbar_init();
+      if (b < batch)
+#pragma unroll
+        for (int k = 0; k < F::NX; ++k) F::issue(&tmap, b, k, smem_u32(sm));
+    }
+    __syncthreads();
+  }
   if (SplitStaging<W, LOGQ, LE, K, INV>::ON && threadIdx.x == 0 && b < batch) split_issue_own<W, LOGQ, LE, K, INV>(st.map, b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
   for (uint32_t it = 0; b < batch; b += groups, ++it) {
     const size_t boff = b * (size_t)K * Sh::Q;
     st.phase = it & 1;
     st.b = b;
     st.next_b = b + groups;
+    if constexpr (FWD_TMA) {
+      // the Q-word buffer takes chunks NX..NX+3 once the previous transform's store has read it
+      if (threadIdx.x == 0) {
+        bulk_wait_read0();
+#pragma unroll
+        for (int k = F::NX; k < F::NX + F::NB; ++k) F::issue(&tmap, b, k, smem_u32(sm));
+      }
+    }
     constexpr int r0 = INV ? Sh::R - 1 : 0;
     split_round<W, LOGQ, LE, K, INV, PLO1, PW, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster, st);
     if constexpr (INV) {
@@ -396,7 +478,9 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   constexpr int LOGQ = LOGL - (K == 4 ? 2 : 1);
   constexpr int LE = SplitLE<W, K>::value;
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
-  const size_t smem = (size_t)Sh::Q * sizeof(W) + (SplitStaging<W, LOGQ, LE, K, INV>::ON ? NTT_SMEM_ALIGN_SLACK + 64 : 0);
+  constexpr bool FWD_TMA = !INV && K == 2;
+  const size_t smem = FWD_TMA ? SplitFwd<W, LOGQ, LE>::SMEM
+                              : (size_t)Sh::Q * sizeof(W) + (SplitStaging<W, LOGQ, LE, K, INV>::ON ? NTT_SMEM_ALIGN_SLACK + 64 : 0);
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   // 2-D tensor map of 128-byte rows over the array the first round reads its own block from
@@ -406,7 +490,8 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   cuuint64_t dims[2] = {(cuuint64_t)ROW_WORDS, (cuuint64_t)(batch * K * (size_t)Sh::Q / ROW_WORDS)};
   cuuint64_t strides[1] = {128};
   constexpr int ROWS = Sh::Q / ROW_WORDS;
-  cuuint32_t box[2] = {(cuuint32_t)ROW_WORDS, (cuuint32_t)(ROWS < 256 ? ROWS : 256)};
+  cuuint32_t box[2] = {(cuuint32_t)ROW_WORDS,
+                       (cuuint32_t)(FWD_TMA ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256))};
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, src, dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
