@@ -68,31 +68,35 @@ struct PwArgs {
   uint64_t J, K, Kp;  // REDC constant and the Shoup constant restoring scale (beta L^{-1} mod p)
 };
 
-// Shared-memory staging of a transform (inverse only): this CTA's block of Q words, the
-// mbarrier right after it.  The forward reads both blocks straight from global memory in its
-// first round: measured faster than staging its own block (u32 2^16: 0.318 vs 0.320 ms,
-// u64 2^15: 0.203 vs 0.216 ms), since the other block's loads expose the same latency.
-template <class W, int LOGQ, int LE, int K, bool INV> struct SplitStaging {
+// Shared-memory staging of a transform (inverse only): this CTA's block of Q words in NCH chunks
+// of one TMA box (256 rows of 128 bytes).  K = 2: the first NX = 3 chunks go to spare slots after
+// the Q-word buffer and are loaded for the next transform as soon as this one's first round has
+// read them; the rest land in the buffer once the DSMEM epilogue no longer reads it.  One mbarrier
+// per chunk after the slots.  (K = 4 runs two CTAs per SM: no spare slots, NX = 0.)  Measured
+// (u32 2^16 / u64 2^15 inverse): -3% / -5% against staging the whole block after the epilogue.
+template <class W, int LOGQ, int LE, int K, bool INV, bool PW> struct SplitStaging {
   static constexpr bool ON = INV;
   static constexpr int Q = 1 << LOGQ;
-  static constexpr int WORDS = Q;
+  static constexpr uint32_t BYTES = (uint32_t)(Q * sizeof(W));
+  static constexpr int ROWS = (int)(BYTES / 128), BOX = ROWS < 256 ? ROWS : 256, NCH = ROWS / BOX;
+  static constexpr uint32_t CH = BOX * 128;
+  static constexpr int CW = (int)(CH / sizeof(W));  // words per chunk
+  // (PW keeps the L1 large: its b operand streams through it with LDG.128, and spare slots that
+  // shrink the L1 carveout made the fused convolution slower: 3 slots +20%, 2 +6%, 1 +2%)
+  static constexpr int NX = (K == 2 && NCH == 4 && !PW) ? 3 : 0;
+  static constexpr uint32_t X_OFF = BYTES, BAR_OFF = X_OFF + NX * CH;
+  static constexpr size_t SMEM = BAR_OFF + 8 * NCH;
+  __device__ static constexpr uint32_t slot(int k) { return k < NX ? X_OFF + k * CH : k * CH; }
+  __device__ static uint32_t bar(uint32_t sbase, int k) { return sbase + BAR_OFF + 8 * k; }
+  // chunks [k0, k1) of this CTA's block of transform b
+  __device__ static void issue(const CUtensorMap* map, size_t b, int rank, int k0, int k1, uint32_t sbase) {
+    const int row0 = (int)((b * K + (size_t)rank) * (size_t)ROWS);
+    for (int k = k0; k < k1; ++k) {
+      mbar_expect_tx(bar(sbase, k), CH);
+      tma_load_2d(sbase + slot(k), map, 0, row0 + k * BOX, bar(sbase, k));
+    }
+  }
 };
-
-template <class W, int LOGQ, int LE, int K, bool INV>
-__device__ __forceinline__ uint32_t split_bar(const W* sm) {
-  return smem_u32(sm) + (uint32_t)(SplitStaging<W, LOGQ, LE, K, INV>::WORDS * sizeof(W));
-}
-
-// TMA loads of the staging of transform b (Q*sizeof(W)/128 rows of 128 bytes per block).
-template <class W, int LOGQ, int LE, int K, bool INV>
-__device__ __forceinline__ void split_issue_own(const CUtensorMap* map, size_t b, int rank, uint32_t dst, uint32_t bar) {
-  using St = SplitStaging<W, LOGQ, LE, K, INV>;
-  constexpr int ROWS = St::Q * (int)sizeof(W) / 128, BOX = ROWS < 256 ? ROWS : 256;
-  const int row0 = (int)((b * K + (size_t)rank) * (size_t)ROWS);
-  mbar_expect_tx(bar, (uint32_t)(St::WORDS * sizeof(W)));
-#pragma unroll
-  for (int bx = 0; bx < ROWS / BOX; ++bx) tma_load_2d(dst + bx * BOX * 128, map, 0, row0 + bx * BOX, bar);
-}
 
 // Staging state of the current transform: the 2-D map (128-byte rows) over x (forward,
 // plain inverse) or a (PW), the mbarrier parity to wait for, and the cluster's next
@@ -202,8 +206,6 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
   constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
   if constexpr (first) {
-    // inverse: this CTA's block of the transform has been staged in shared memory
-    if constexpr (INV) mbar_wait(split_bar<W, LOGQ, LE, K, INV>(sm), st.phase);
     if constexpr (!INV && K == 2) {
       // stage 1 (m = L/2) on x_j and x_{j+Q}: CTA 0 keeps the sums (Algorithm 3 lines 1-2), CTA 1
       // the twiddled differences (lines 3-5, W = zeta_1^j).  The CTA-uniform choice is made outside
@@ -252,6 +254,11 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // this CTA's block of the bit-reversed input (contiguous runs, from shared memory);
       // PW: c = a b L^{-1} with b read from global memory 16 bytes at a time
       constexpr int PER = 16 / (int)sizeof(W);
+      using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
+      if constexpr (PW) {  // the whole block staged first (measured: 1.5% faster than overlapping the waits)
+#pragma unroll
+        for (int k = 0; k < St::NCH; ++k) mbar_wait(St::bar(smem_u32(sm), k), st.phase);
+      }
       if constexpr (PW) {  // every b load in flight first (into v itself), then combine with a
 #pragma unroll
         for (int q = 0; q < G; ++q)
@@ -262,12 +269,18 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
                         v + q * S + h);
           }
       }
+      // this CTA's block of the transform has been staged in shared memory (without PW each group
+      // waits for the chunk its run lies in)
+      static_assert(St::CW % S == 0, "runs do not straddle chunks");
 #pragma unroll
       for (int q = 0; q < G; ++q) {
+        const int e0 = blk[q] * S, k = e0 / St::CW;
+        if constexpr (!PW) mbar_wait(St::bar(smem_u32(sm), k), st.phase);
+        const W* src = reinterpret_cast<const W*>(reinterpret_cast<const unsigned char*>(sm) + St::slot(k)) - k * St::CW;
 #pragma unroll
         for (int h = 0; h < S; h += PER) {
           W av[PER];
-          unpack16<W>(lds128(sm + tswz<W>(blk[q] * S + h)), av);
+          unpack16<W>(lds128(src + tswz<W>(e0 + h)), av);
           if constexpr (PW) {
 #pragma unroll
             for (int e = 0; e < PER; ++e) {
@@ -386,7 +399,12 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     if constexpr (!INV) {
       if (threadIdx.x == 0) bulk_wait_read0();
     }
+    using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
+    if constexpr (INV && first && St::NX > 0) fence_proxy_async_smem();
     __syncthreads();
+    if constexpr (INV && first && St::NX > 0) {  // the spare slots take the next transform's chunks
+      if (threadIdx.x == 0 && st.next_b < st.batch) St::issue(st.map, st.next_b, rank, 0, St::NX, smem_u32(sm));
+    }
 #pragma unroll
     for (int q = 0; q < G; ++q)
 #pragma unroll
@@ -404,23 +422,18 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
              const TwPair<W>* __restrict__ tw_full, W p, PwArgs pw) {
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // staged (inverse): 1024-byte alignment for the TMA swizzle period (same offset in every
-  // CTA of the cluster); the forward keeps the plain Q-word buffer (measured: its extra
-  // 1 KiB of shared memory costs the forward 15%, through the L1 carveout)
-  unsigned char* base = smem_raw;
-  if constexpr (SplitStaging<W, LOGQ, LE, K, INV>::ON) {
-    const uint32_t s0 = smem_u32(smem_raw);
-    base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
-  }
-  W* sm = reinterpret_cast<W*>(base);
+  // dynamic shared memory starts 1024-byte aligned (tma.cuh), as the TMA swizzle period needs
+  W* sm = reinterpret_cast<W*>(smem_raw);
+  using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int t = threadIdx.x;
   const Mod<W> m = make_mod<W>(p);
   SplitStage st{&tmap, 0u, 0, 0, batch};
-  if constexpr (SplitStaging<W, LOGQ, LE, K, INV>::ON) {
+  if constexpr (St::ON) {
     if (threadIdx.x == 0) {
-      mbar_init(split_bar<W, LOGQ, LE, K, INV>(sm), 1);
+#pragma unroll
+      for (int k = 0; k < St::NCH; ++k) mbar_init(St::bar(smem_u32(sm), k), 1);
       fence_mbar_init();
     }
     __syncthreads();
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     }
     __syncthreads();
   }
-  if (SplitStaging<W, LOGQ, LE, K, INV>::ON && threadIdx.x == 0 && b < batch) split_issue_own<W, LOGQ, LE, K, INV>(st.map, b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
+  if (St::ON && threadIdx.x == 0 && b < batch) St::issue(st.map, b, rank, 0, St::NCH, smem_u32(sm));
   for (uint32_t it = 0; b < batch; b += groups, ++it) {
     const size_t boff = b * (size_t)K * Sh::Q;
     st.phase = it & 1;
@@ -461,8 +474,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
       // after the epilogue's cluster barrier no CTA reads this buffer any more
       fence_proxy_async_smem();
       __syncthreads();
-      if (threadIdx.x == 0 && st.next_b < batch)
-        split_issue_own<W, LOGQ, LE, K, INV>(st.map, st.next_b, rank, smem_u32(sm), split_bar<W, LOGQ, LE, K, INV>(sm));
+      if (threadIdx.x == 0 && st.next_b < batch) St::issue(st.map, st.next_b, rank, St::NX, St::NCH, smem_u32(sm));
     }
     __syncthreads();
   }
@@ -480,7 +492,8 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   constexpr bool FWD_TMA = !INV && K == 2;
   const size_t smem = FWD_TMA ? SplitFwd<W, LOGQ, LE>::SMEM
-                              : (size_t)Sh::Q * sizeof(W) + (SplitStaging<W, LOGQ, LE, K, INV>::ON ? NTT_SMEM_ALIGN_SLACK + 64 : 0);
+                              : (SplitStaging<W, LOGQ, LE, K, INV, PW>::ON ? SplitStaging<W, LOGQ, LE, K, INV, PW>::SMEM
+                                                                       : (size_t)Sh::Q * sizeof(W));
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   // 2-D tensor map of 128-byte rows over the array the first round reads its own block from
