@@ -111,7 +111,10 @@ ntt_status ntt_pointwise_mul(ntt_plan_t plan, void* c, const void* a, const void
 
 /* Cyclic convolution of `batch` pairs (config C3 building block): a <- a * b
  * (cyclic, length L, mod p).  Runs forward(a), forward(b), pointwise with
- * L^{-1}, inverse(a); b is overwritten by its transform.  Inputs in [0,2p). */
+ * L^{-1}, inverse(a).  For the 2-CTA cluster sizes (L = 2^16 u32, 2^15 u64) the
+ * product is fused into the last round of b's forward, which then only reads b;
+ * otherwise b is overwritten by its transform: b's contents are unspecified on
+ * return.  Inputs in [0,2p). */
 ntt_status ntt_cyclic_convolve(ntt_plan_t plan, void* a, void* b, size_t batch, ntt_stream_t stream);
 
 /* Host-resident data (end-to-end use): ops is a bit set of NTT_OP_FORWARD and

@@ -20,6 +20,10 @@
 // pointwise product c = a b L^{-1} is formed while loading, so a cyclic
 // convolution needs no separate pointwise pass.
 //
+// Forward with PW (cyclic convolution): the last round multiplies b-hat (registers) by this
+// CTA's block of a-hat, staged by TMA into the Q-word buffer while the round computes, and the
+// product c-hat = a-hat b-hat L^{-1} leaves over a-hat; b is only read, so no cluster barrier.
+//
 // Staging (inverse): each CTA's own block of the next transform (x, or a when PW) is
 // brought into shared memory by TMA (2-D tensor map of 128-byte rows, SWIZZLE_128B) once
 // the cluster's DSMEM epilogue no longer reads the buffer; the first round then reads it
@@ -106,6 +110,7 @@ struct SplitStage {
   const CUtensorMap* map;
   uint32_t phase;
   size_t b, next_b, batch;
+  const CUtensorMap* map_a;  // forward with PW: 128-byte rows of a (a-hat in, c-hat out)
 };
 
 #ifndef NTT_SPLIT_NX
@@ -217,7 +222,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // arrive here, wait only before the last round's in-place store.  Measured against a full
       // cluster.sync() at this point: u32 2^16 -7%, u64 2^15 -3% (the wait no longer stalls the
       // early CTA, and cluster.sync's MEMBAR.GPU + L1 invalidate are gone).
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      if constexpr (!PW) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     } else if constexpr (!INV) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
@@ -302,12 +307,47 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
       for (int h = 0; h < S; ++h) v[q * S + h] = sm[sswz<W>(blk[q] * B + h * D + c[q])];
   }
+  if constexpr (PW && !INV && last) {
+    // forward with the pointwise product: every thread has its last-round inputs, so the buffer
+    // takes this CTA's block of a-hat (TMA) while the round computes
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      using F = SplitFwd<W, LOGQ, LE>;
+      constexpr int ROWS = Q * (int)sizeof(W) / 128;
+      const uint32_t abar = smem_u32(sm) + (uint32_t)F::SMEM;
+      const int row0 = (int)((st.b * K + (size_t)rank) * (size_t)ROWS);
+      mbar_expect_tx(abar, (uint32_t)(Q * sizeof(W)));
+#pragma unroll
+      for (int bx = 0; bx < ROWS / F::BOXR; ++bx)
+        tma_load_2d(smem_u32(sm) + bx * F::BOXR * 128, st.map_a, 0, row0 + bx * F::BOXR, abar);
+    }
+  }
   if constexpr (!INV) dif_round<W, LOGQ, SR, LEVEL, G, PLO1>(v, c, tw_sub, m);
   else dit_round<W, LOGQ, SR, LEVEL, G, PLO1>(v, c, tw_sub, m);
   if constexpr (last) {
     if constexpr (!INV) {
+      if constexpr (PW) {
+        // c-hat = a-hat b-hat L^{-1} with b-hat in [0,2p) straight from the registers; c-hat in
+        // [0,2p) is a valid inverse input (Algorithm 4 takes [0,4p))
+        mbar_wait(smem_u32(sm) + (uint32_t)SplitFwd<W, LOGQ, LE>::SMEM, st.phase);
+        constexpr int PER = 16 / (int)sizeof(W);
 #pragma unroll
-      for (int i = 0; i < Sh::E; ++i) v[i] = norm2<W>(v[i], m.p);
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+          for (int h = 0; h < S; h += PER) {
+            W av[PER];
+            unpack16<W>(lds128(sm + tswz<W>(blk[q] * S + h)), av);
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+              W prod = mont_redc_mul<W>(av[e], v[q * S + h + e], (W)pw.J, m.p);
+              v[q * S + h + e] = shoup_mul<W>(prod, (W)pw.K, (W)pw.Kp, m.p);
+            }
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < Sh::E; ++i) v[i] = norm2<W>(v[i], m.p);
+      }
       // out through shared memory in the TMA 128-byte-swizzled layout and one bulk tensor store
       // of the block: per-thread strided 16-byte global stores congested the LSU (lg_throttle, and
       // long-scoreboard waits on the stores' source registers)
@@ -320,13 +360,15 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         for (int h = 0; h < S; h += PER) sts128(sm + tswz<W>(blk[q] * S + h), pack16<W>(v + q * S + h));
       fence_proxy_async_smem();
       __syncthreads();
-      if constexpr (K == 2) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // partner read x_b
+      // partner read x_b (PW: x is only read; c-hat goes to a's block, read only by this CTA)
+      if constexpr (K == 2 && !PW) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
       if (threadIdx.x == 0) {
         constexpr int ROWS = Q * (int)sizeof(W) / 128;
         constexpr int BOX = (K == 2) ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256);
         const int row0 = (int)((st.b * K + (size_t)rank) * (size_t)ROWS);
+        const CUtensorMap* omap = PW ? st.map_a : st.map;
 #pragma unroll
-        for (int bx = 0; bx < ROWS / BOX; ++bx) tma_store_2d(st.map, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
+        for (int bx = 0; bx < ROWS / BOX; ++bx) tma_store_2d(omap, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
         bulk_commit();
       }
     } else {
@@ -418,7 +460,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW>
 __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
                                   SplitShape<LOGQ, LE, K, (int)sizeof(W)>::MINB)
-    k_splitk(const __grid_constant__ CUtensorMap tmap, W* __restrict__ x, size_t batch,
+    k_splitk(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_a, W* __restrict__ x,
+             size_t batch,
              const TwPair<W>* __restrict__ tw_full, W p, PwArgs pw) {
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -429,7 +472,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
   const int rank = (int)cluster.block_rank();
   const int t = threadIdx.x;
   const Mod<W> m = make_mod<W>(p);
-  SplitStage st{&tmap, 0u, 0, 0, batch};
+  SplitStage st{&tmap, 0u, 0, 0, batch, &tmap_a};
   if constexpr (St::ON) {
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -447,6 +490,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < F::NCH; ++k) mbar_init(smem_u32(sm) + F::BAR_OFF + 8 * k, 1);
+      if constexpr (PW) mbar_init(smem_u32(sm) + (uint32_t)F::SMEM, 1);  // a-hat staging
       fence_mbar_init();
       if (b < batch)
 #pragma unroll
@@ -491,25 +535,28 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   constexpr int LE = SplitLE<W, K>::value;
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   constexpr bool FWD_TMA = !INV && K == 2;
-  const size_t smem = FWD_TMA ? SplitFwd<W, LOGQ, LE>::SMEM
+  const size_t smem = FWD_TMA ? SplitFwd<W, LOGQ, LE>::SMEM + (PW ? 8 : 0)
                               : (SplitStaging<W, LOGQ, LE, K, INV, PW>::ON ? SplitStaging<W, LOGQ, LE, K, INV, PW>::SMEM
                                                                        : (size_t)Sh::Q * sizeof(W));
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  // 2-D tensor map of 128-byte rows over the array the first round reads its own block from
-  void* src = PW ? const_cast<void*>(pw.a) : x;
+  // 2-D tensor maps of 128-byte rows: map over the array the first round reads (x; a for the
+  // inverse with PW), map_a over a for the forward with PW (a-hat in, c-hat out)
   constexpr int ROW_WORDS = 128 / (int)sizeof(W);
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)ROW_WORDS, (cuuint64_t)(batch * K * (size_t)Sh::Q / ROW_WORDS)};
-  cuuint64_t strides[1] = {128};
   constexpr int ROWS = Sh::Q / ROW_WORDS;
-  cuuint32_t box[2] = {(cuuint32_t)ROW_WORDS,
-                       (cuuint32_t)(FWD_TMA ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256))};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, src, dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  CUtensorMap maps[2];
+  void* srcs[2] = {(INV && PW) ? const_cast<void*>(pw.a) : x, PW ? const_cast<void*>(pw.a) : x};
+  for (int i = 0; i < 2; ++i) {
+    cuuint64_t dims[2] = {(cuuint64_t)ROW_WORDS, (cuuint64_t)(batch * K * (size_t)Sh::Q / ROW_WORDS)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {(cuuint32_t)ROW_WORDS,
+                         (cuuint32_t)(FWD_TMA ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256))};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&maps[i], sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                      srcs[i], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   auto kern = k_splitk<W, LOGQ, LE, K, INV, PLO1, PW>;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -539,7 +586,7 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, map, reinterpret_cast<W*>(x), batch,
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], reinterpret_cast<W*>(x), batch,
                             reinterpret_cast<const TwPair<W>*>(tw), (W)p, pw);
 }
 
@@ -568,11 +615,16 @@ static cudaError_t run_split_k(void* x, size_t batch, const void* tw, uint64_t p
 cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
                           const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s) {
   PwArgs pw{pw_a, pw_b, J, K, Kp};
+  // fused (pw_a set): inverse -- a <- InvNTT(a * b L^{-1}); forward -- a <- NTT(x) * a L^{-1}, x only
+  // read (K = 2 only)
   const bool fused = pw_a != nullptr;
+  if (fused && !inverse && split_k() != 2) return cudaErrorNotSupported;
   if (wbytes == 8) {
     if (logn != kContigMaxLog64 + 1) return cudaErrorInvalidValue;
     constexpr int L = kContigMaxLog64 + 1;
     const bool plo1 = (p & 0xffffffffull) == 1;
+    if (!inverse && fused) return plo1 ? run_split<uint64_t, L, 2, false, true, true>(x, batch, tw, p, pw, s)
+                                       : run_split<uint64_t, L, 2, false, false, true>(x, batch, tw, p, pw, s);
     if (!inverse) return plo1 ? run_split_k<uint64_t, L, false, true, false>(x, batch, tw, p, pw, s)
                               : run_split_k<uint64_t, L, false, false, false>(x, batch, tw, p, pw, s);
     if (fused) return plo1 ? run_split_k<uint64_t, L, true, true, true>(x, batch, tw, p, pw, s)
@@ -582,6 +634,7 @@ cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t ba
   }
   if (logn != kContigMaxLog32 + 1) return cudaErrorInvalidValue;
   constexpr int L = kContigMaxLog32 + 1;
+  if (!inverse && fused) return run_split<uint32_t, L, 2, false, false, true>(x, batch, tw, p, pw, s);
   if (!inverse) return run_split_k<uint32_t, L, false, false, false>(x, batch, tw, p, pw, s);
   if (fused) return run_split_k<uint32_t, L, true, false, true>(x, batch, tw, p, pw, s);
   return run_split_k<uint32_t, L, true, false, false>(x, batch, tw, p, pw, s);

@@ -711,6 +711,22 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, nt
   unsigned total = 0;
   ntt_status st = ntt_forward(pl, a, batch, stream);
   total += t_launches;
+  static const bool inv_pw = getenv("NTT_CONV_INV_PW") != nullptr;  // A/B hook: product fused into the inverse
+  if (st == NTT_OK && batch && !inv_pw && pl->passes.size() == 1 && pl->bfly == NTT_BFLY_ALG3 &&
+      nttb::split2_supported((int)pl->wbytes, (int)pl->ell) && aligned16(b)) {
+    // forward of b with the pointwise product (x L^{-1}) fused into its last round, written over
+    // a-hat; then the plain inverse of a.  b is only read.
+    DeviceGuard g(pl->device);
+    cudaError_t e = nttb::launch_split2((int)pl->wbytes, (int)pl->ell, false, b, batch, pl->tw_fwd, pl->p, a, b, pl->J,
+                                        pl->K_scale, pl->Kp_scale, (cudaStream_t)stream);
+    if (e != cudaErrorNotSupported) {
+      if (e != cudaSuccess) return cuda_fail(e);
+      st = ntt_inverse(pl, a, batch, stream);
+      t_launches += total + 1;
+      return st;
+    }
+    cudaGetLastError();
+  }
   if (st == NTT_OK) { st = ntt_forward(pl, b, batch, stream); total += t_launches; }
   if (st == NTT_OK && pl->passes.size() == 1 && nttb::split2_supported((int)pl->wbytes, (int)pl->ell)) {
     // pointwise product (x L^{-1}) fused into the inverse's load

@@ -457,7 +457,8 @@ def test_execute_host_pipeline(ntt, bits, p, ell, batch, buf_transforms):
                            ref.cpu().view(torch.int64 if bits == 64 else torch.int32)), ops
 
 
-@pytest.mark.parametrize("bits,p,ell,batch", [(64, P62, 12, 9), (64, P62, 17, 2), (32, P30, 11, 5)])
+@pytest.mark.parametrize("bits,p,ell,batch", [(64, P62, 12, 9), (64, P62, 17, 2), (32, P30, 11, 5),
+                                               (64, P62, 15, 77), (64, P62G, 15, 3), (32, RNS[1], 16, 75)])
 def test_cyclic_convolution_other_shapes(ntt, bits, p, ell, batch):
     """ntt_cyclic_convolve beyond C3's shape (single-pass u64, multi-pass with separate pointwise): each
     pair against the oracle's per-coefficient definition on sampled k and the oracle NTT route."""
