@@ -104,8 +104,14 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
     (void)xb;
     (void)active;
   } else {
-    __syncthreads();
-    if (first_exchange && threadIdx.x == 0 && next_tile < ntiles) {
+    // forward: the exchange into the last round (contiguous runs) is warp-local when the previous
+    // round's blocks fit a warp (rounds.cuh) -- warps then skew freely instead of meeting twice per
+    // tile.  (The inverse's first exchange carries the next tile's prefetch and stays CTA-wide.)
+    constexpr int nr = INV ? r - 1 : r + 1;
+    constexpr bool WL = !INV && warp_local_exchange<LOGN, LE, r, nr>();
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
+    if (!WL && first_exchange && threadIdx.x == 0 && next_tile < ntiles) {
       // every thread has finished the previous tile (the other buffer): once its TMA
       // store has read the buffer, prefetch the next tile into it
       bulk_wait_read0();
@@ -127,8 +133,8 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
         for (int h = 0; h < S; ++h) sb[tswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
       }
     }
-    __syncthreads();
-    constexpr int nr = INV ? r - 1 : r + 1;
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
     tma_round<W, LOGN, LE, INV, PLO1, BF, nr>(v, xb, sb, t, active, tw, m, norm, false, map, next_tile, ntiles,
                                               next_buf, next_bar);
   }

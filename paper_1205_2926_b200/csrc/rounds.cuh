@@ -45,6 +45,20 @@ template <int LOGN, int LE> struct Rounds {
   }
 };
 
+// True when the exchange between rounds ra and rb of an N = 2^LOGN transform with T = N/2^LE
+// threads stays inside each warp: one round holds contiguous runs (D = 1), the other one group
+// (G = 1) of the same run length S per thread with D <= 32 dividing 32, so warp w holds the
+// elements [32 S w, 32 S (w+1)) in both.  Such an exchange needs __syncwarp, not __syncthreads.
+template <int LOGN, int LE, int ra, int rb> __host__ __device__ constexpr bool warp_local_exchange() {
+  using RC = Rounds<LOGN, LE>;
+  constexpr int N = 1 << LOGN, T = N >> LE;
+  constexpr int Sa = 1 << RC::sr(ra), Sb = 1 << RC::sr(rb);
+  constexpr int Da = N >> (RC::level(ra) + RC::sr(ra)), Db = N >> (RC::level(rb) + RC::sr(rb));
+  constexpr bool G1 = (Sa == (1 << LE)) && (Sb == (1 << LE));
+  constexpr bool runs = (Da == 1 && Db <= 32 && 32 % Db == 0) || (Db == 1 && Da <= 32 && 32 % Da == 0);
+  return T % 32 == 0 && G1 && runs;
+}
+
 // Forward round: stages LEVEL+1 .. LEVEL+SR with the Algorithm 3 butterfly.
 // Butterflies known at compile time to have W = 1 (the whole last stage, m = 1, and
 // every k = 0 butterfly of a round with D = 1) take the multiply-free path.
