@@ -104,14 +104,17 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
     (void)xb;
     (void)active;
   } else {
-    // forward: the exchange into the last round (contiguous runs) is warp-local when the previous
-    // round's blocks fit a warp (rounds.cuh) -- warps then skew freely instead of meeting twice per
-    // tile.  (The inverse's first exchange carries the next tile's prefetch and stays CTA-wide.)
+    // The exchange between the contiguous-run round and its neighbour is warp-local when that
+    // round's blocks fit a warp (rounds.cuh): warps then skew freely instead of meeting twice per
+    // tile.  The next tile's prefetch needs a CTA-wide barrier, so it rides on the forward's first
+    // exchange and on the inverse's last one.
     constexpr int nr = INV ? r - 1 : r + 1;
-    constexpr bool WL = !INV && warp_local_exchange<LOGN, LE, r, nr>();
+    constexpr bool PREFETCH = INV ? (nr == 0) : (r == 0);
+    constexpr bool WL = !PREFETCH && warp_local_exchange<LOGN, LE, r, nr>();
+    (void)first_exchange;
     if constexpr (WL) __syncwarp();
     else __syncthreads();
-    if (!WL && first_exchange && threadIdx.x == 0 && next_tile < ntiles) {
+    if (PREFETCH && threadIdx.x == 0 && next_tile < ntiles) {
       // every thread has finished the previous tile (the other buffer): once its TMA
       // store has read the buffer, prefetch the next tile into it
       bulk_wait_read0();
