@@ -292,9 +292,24 @@ __global__ void __launch_bounds__(ColsShape<W, LOGN, LE>::THREADS, ColsShape<W, 
 // without scaling) restores the scale; then normalise.
 template <class W>
 __global__ void k_pointwise(W* __restrict__ c, const W* __restrict__ a, const W* __restrict__ b, size_t n, W p, W J,
-                            W K, W Kp) {
+                            W K, W Kp, int vec) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t done = 0;
+  if (vec) {  // 16-byte vectors (all three pointers 16-byte aligned), streaming loads and stores
+    constexpr int PER = 16 / (int)sizeof(W);
+    const size_t nv = n / PER;
+    for (size_t i = i0; i < nv; i += stride) {
+      W av[PER], bv[PER], cv[PER];
+      unpack16<W>(__ldcs(reinterpret_cast<const uint4*>(a) + i), av);
+      unpack16<W>(__ldcs(reinterpret_cast<const uint4*>(b) + i), bv);
+#pragma unroll
+      for (int e = 0; e < PER; ++e) cv[e] = norm2<W>(shoup_mul<W>(mont_redc_mul<W>(av[e], bv[e], J, p), K, Kp, p), p);
+      __stcs(reinterpret_cast<uint4*>(c) + i, pack16<W>(cv));
+    }
+    done = nv * PER;
+  }
+  for (size_t i = done + i0; i < n; i += stride) {
     W r = mont_redc_mul<W>(a[i], b[i], J, p);
     r = shoup_mul<W>(r, K, Kp, p);
     c[i] = norm2<W>(r, p);
@@ -579,13 +594,15 @@ cudaError_t launch_pointwise(int wbytes, void* c, const void* a, const void* b, 
                              uint64_t K, uint64_t Kp, cudaStream_t s) {
   if (!n) return cudaSuccess;
   const int th = 256;
+  const int vec = (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15) == 0;
+  const size_t nthreads = vec ? n / (16 / wbytes) + 1 : n;
   if (wbytes == 8)
-    k_pointwise<uint64_t><<<elementwise_grid(n, th), th, 0, s>>>((uint64_t*)c, (const uint64_t*)a, (const uint64_t*)b,
-                                                                   n, p, J, K, Kp);
+    k_pointwise<uint64_t><<<elementwise_grid(nthreads, th), th, 0, s>>>(
+        (uint64_t*)c, (const uint64_t*)a, (const uint64_t*)b, n, p, J, K, Kp, vec);
   else
-    k_pointwise<uint32_t><<<elementwise_grid(n, th), th, 0, s>>>((uint32_t*)c, (const uint32_t*)a, (const uint32_t*)b,
-                                                                   n, (uint32_t)p, (uint32_t)J, (uint32_t)K,
-                                                                   (uint32_t)Kp);
+    k_pointwise<uint32_t><<<elementwise_grid(nthreads, th), th, 0, s>>>(
+        (uint32_t*)c, (const uint32_t*)a, (const uint32_t*)b, n, (uint32_t)p, (uint32_t)J, (uint32_t)K, (uint32_t)Kp,
+        vec);
   return cudaGetLastError();
 }
 
