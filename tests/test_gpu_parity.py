@@ -225,6 +225,56 @@ def test_pointwise(ntt):
             plan.pointwise_mul(dc, da, db, scale_inv_L=scale)
             ref = oracle.pointwise(p, a, b, scale_L=L if scale else 0)
             assert np.array_equal(to_host(dc), ref)
+        # word-aligned but not 16-byte-aligned views (the scalar path of k_pointwise), and L = 2 with an
+        # odd batch (the 16-byte path's tail)
+        fa, fb = to_dev(a.reshape(-1), bits), to_dev(b.reshape(-1), bits)
+        out = torch.zeros(4 * L + 1, dtype=fa.dtype, device="cuda")
+        plan.pointwise_mul(out[1:L + 1], fa[1:L + 1], fb[1:L + 1], batch=1, scale_inv_L=True)
+        assert np.array_equal(to_host(out[1:L + 1]),
+                              oracle.pointwise(p, a.reshape(-1)[1:L + 1], b.reshape(-1)[1:L + 1], scale_L=L))
+        rest = to_host(out)
+        assert rest[0] == 0 and not rest[L + 1:].any(), "pointwise wrote outside its view"
+        plan2 = ntt.Plan(p, root(p, 2), 1, bits)
+        a2, b2 = rand_residues(rng, 2 * p, (7, 2)), rand_residues(rng, 2 * p, (7, 2))
+        dc2 = torch.empty(14, dtype=fa.dtype, device="cuda")
+        plan2.pointwise_mul(dc2, to_dev(a2, bits), to_dev(b2, bits))
+        assert np.array_equal(to_host(dc2).reshape(7, 2), oracle.pointwise(p, a2, b2, scale_L=0))
+
+
+def test_convolution_inverse_fused_variant(ntt, tmp_path):
+    """The alternative cluster-size convolution (product fused into the inverse's load: NTT_CONV_INV_PW, read
+    once per process, so run in a child process) equals the default path (product fused into b's forward)."""
+    import os
+    import subprocess
+    import sys
+    for bits, p, ell, batch in ((32, RNS[2], 16, 77), (64, P62, 15, 5)):
+        L = 1 << ell
+        rng = np.random.default_rng(bits + batch)
+        a = rand_residues(rng, p, (batch, L))
+        b = rand_residues(rng, p, (batch, L))
+        np.save(tmp_path / "a.npy", a)
+        np.save(tmp_path / "b.npy", b)
+        child = (
+            "import sys, numpy as np, torch; sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})\n"
+            "import paper_1205_2926_b200 as ntt\nfrom gpu_util import root, to_dev, to_host\n"
+            "a = np.load({pa!r}); b = np.load({pb!r})\n"
+            "plan = ntt.Plan({p}, root({p}, {L}), {ell}, {bits})\n"
+            "da, db = to_dev(a, {bits}), to_dev(b, {bits}); plan.cyclic_convolve(da, db)\n"
+            "np.save({out!r}, to_host(da))\n"
+        ).format(root=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                 tests=os.path.dirname(os.path.abspath(__file__)), pa=str(tmp_path / "a.npy"),
+                 pb=str(tmp_path / "b.npy"), p=p, L=L, ell=ell, bits=bits, out=str(tmp_path / "c.npy"))
+        env = dict(os.environ, NTT_CONV_INV_PW="1")
+        r = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        alt = np.load(tmp_path / "c.npy")
+        plan = ntt.Plan(p, root(p, L), ell, bits)
+        da, db = to_dev(a, bits), to_dev(b, bits)
+        plan.cyclic_convolve(da, db)
+        assert np.array_equal(to_host(da), alt)
+        for i in (0, batch - 1):
+            for k in (0, L - 1):
+                assert int(alt[i, k]) == oracle.cyclic_conv_coeff(p, a[i], b[i], k)
 
 
 def test_twiddle_table(ntt):
