@@ -441,9 +441,13 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     if constexpr (!INV) {
       if (threadIdx.x == 0) bulk_wait_read0();
     }
+    // forward: the exchange into the last round is warp-local when its blocks fit a warp (rounds.cuh)
+    constexpr int nr_ = INV ? r - 1 : r + 1;
+    constexpr bool WL = !INV && warp_local_exchange<LOGQ, LE, r, nr_>();
     using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
     if constexpr (INV && first && St::NX > 0) fence_proxy_async_smem();
-    __syncthreads();
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
     if constexpr (INV && first && St::NX > 0) {  // the spare slots take the next transform's chunks
       if (threadIdx.x == 0 && st.next_b < st.batch) St::issue(st.map, st.next_b, rank, 0, St::NX, smem_u32(sm));
     }
@@ -451,7 +455,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     for (int q = 0; q < G; ++q)
 #pragma unroll
       for (int h = 0; h < S; ++h) sm[sswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
-    __syncthreads();
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
     split_round<W, LOGQ, LE, K, INV, PLO1, PW, nr>(v, xb, sm, t, rank, tw_full, m, pw, boff, cluster, st);
   }
