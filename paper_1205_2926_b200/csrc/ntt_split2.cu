@@ -441,14 +441,18 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     if constexpr (!INV) {
       if (threadIdx.x == 0) bulk_wait_read0();
     }
-    // forward: the exchange into the last round is warp-local when its blocks fit a warp (rounds.cuh)
+    // The exchange next to the contiguous-run round is warp-local when its blocks fit a warp
+    // (rounds.cuh).  The inverse's spare-slot refill needs every thread past its first round (a CTA
+    // barrier): it rides on the first exchange, or on the second when the first is warp-local.
     constexpr int nr_ = INV ? r - 1 : r + 1;
-    constexpr bool WL = !INV && warp_local_exchange<LOGQ, LE, r, nr_>();
+    constexpr bool WL = warp_local_exchange<LOGQ, LE, r, nr_>() && !(INV && Sh::R < 3);
+    constexpr bool FIRST_WL = INV && Sh::R >= 3 && warp_local_exchange<LOGQ, LE, Sh::R - 1, Sh::R - 2>();
     using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
-    if constexpr (INV && first && St::NX > 0) fence_proxy_async_smem();
+    constexpr bool REFILL = INV && St::NX > 0 && (FIRST_WL ? r == Sh::R - 2 : first);
+    if constexpr (REFILL) fence_proxy_async_smem();
     if constexpr (WL) __syncwarp();
     else __syncthreads();
-    if constexpr (INV && first && St::NX > 0) {  // the spare slots take the next transform's chunks
+    if constexpr (REFILL) {  // the spare slots take the next transform's chunks
       if (threadIdx.x == 0 && st.next_b < st.batch) St::issue(st.map, st.next_b, rank, 0, St::NX, smem_u32(sm));
     }
 #pragma unroll
