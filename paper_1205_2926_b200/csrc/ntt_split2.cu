@@ -353,7 +353,10 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // long-scoreboard waits on the stores' source registers)
       static_assert(D == 1, "the forward's last round holds contiguous runs");
       constexpr int PER = 16 / (int)sizeof(W);
-      __syncthreads();  // every thread has read its last-round inputs from sm
+      // every thread has read its last-round inputs from sm (only its own warp's region when the
+      // exchange into this round was warp-local and no a-hat was staged over the buffer)
+      if constexpr (!PW && warp_local_exchange<LOGQ, LE, r - 1, r>()) __syncwarp();
+      else __syncthreads();
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
