@@ -67,7 +67,8 @@ cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize
 // fuses the pointwise product a*b*L^{-1} into the inverse's load (cyclic convolution)
 bool split2_supported(int wbytes, int logn);
 cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
-                          const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s);
+                          const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s,
+                          const void* tw1s = nullptr);
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
                         uint64_t p, cudaStream_t s);
 // the same pass with TMA-staged, double-buffered tiles (ntt_cols_tma.cu)

@@ -70,6 +70,7 @@ struct PwArgs {
   const void* a;
   const void* b;
   uint64_t J, K, Kp;  // REDC constant and the Shoup constant restoring scale (beta L^{-1} mod p)
+  const void* tw1s;   // forward with PW: stage-1 table scaled by K (zeta_1^j K, its W')
 };
 
 // Shared-memory staging of a transform (inverse only): this CTA's block of Q words in NCH chunks
@@ -147,9 +148,12 @@ template <class W, int LOGQ, int LE> struct SplitFwd {
 };
 
 // Stage 1 of the forward from the staged chunks: CTA 0 keeps sums, CTA 1 twiddled differences.
-template <class W, int LOGQ, int LE, int LOGL, bool PLO1, bool UPPER>
+// SCALE (forward with the pointwise product): stage 1 also multiplies by K = beta L^{-1} -- CTA 0's
+// sums by one Shoup product (work CTA 1 already spends on its twiddles), CTA 1's differences through
+// the pre-scaled table -- so the final product needs one REDC instead of REDC + Shoup.
+template <class W, int LOGQ, int LE, int LOGL, bool PLO1, bool UPPER, bool SCALE = false>
 __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const TwPair<W>* __restrict__ tw_full,
-                                                 const Mod<W>& m, const SplitStage& st) {
+                                                 const Mod<W>& m, const SplitStage& st, const PwArgs& pw) {
   using F = SplitFwd<W, LOGQ, LE>;
   const unsigned char* base = reinterpret_cast<const unsigned char*>(sm);
   const uint32_t sbase = smem_u32(sm);
@@ -164,11 +168,14 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
     for (int hh = 0; hh < F::HC; ++hh) {
       const int h = k * F::HC + hh, j = h * F::D + t;
       const W a = lo[hh * F::D + tsw], b = hi[hh * F::D + tsw];
-      if constexpr (!UPPER) {
+      if constexpr (!UPPER && SCALE) {
+        v[h] = shoup_mul<W, PLO1>(a + b, (W)pw.K, (W)pw.Kp, m);  // a + b < 4p < beta: a Shoup input
+      } else if constexpr (!UPPER) {
         v[h] = csub<W>(a + b, m.p2);
       } else {
         W w, wp;
-        ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
+        if constexpr (SCALE) ldtw<W>(reinterpret_cast<const TwPair<W>*>(pw.tw1s), (uint32_t)j, w, wp);
+        else ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
         v[h] = shoup_mul<W, PLO1>(a - b + m.p2, w, wp, m);
       }
     }
@@ -216,8 +223,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // the twiddled differences (lines 3-5, W = zeta_1^j).  The CTA-uniform choice is made outside
       // the element loops so the loads (data and twiddles) are scheduled ahead of their use.
       static_assert(G == 1 && S == SplitFwd<W, LOGQ, LE>::S, "first round: one column per thread");
-      if (rank == 0) split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, false>(v, sm, t, tw_full, m, st);
-      else split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, true>(v, sm, t, tw_full, m, st);
+      if (rank == 0) split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, false, PW>(v, sm, t, tw_full, m, st, pw);
+      else split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, true, PW>(v, sm, t, tw_full, m, st, pw);
       // every CTA has read x_b (the loaded values are consumed, so a relaxed arrive orders them):
       // arrive here, wait only before the last round's in-place store.  Measured against a full
       // cluster.sync() at this point: u32 2^16 -7%, u64 2^15 -3% (the wait no longer stalls the
@@ -328,8 +335,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   if constexpr (last) {
     if constexpr (!INV) {
       if constexpr (PW) {
-        // c-hat = a-hat b-hat L^{-1} with b-hat in [0,2p) straight from the registers; c-hat in
-        // [0,2p) is a valid inverse input (Algorithm 4 takes [0,4p))
+        // c-hat = a-hat b-hat L^{-1} with b-hat (already scaled by beta L^{-1} in stage 1, in
+        // [0,2p)) straight from the registers: one REDC; c-hat in (0,2p) is a valid inverse input
         mbar_wait(smem_u32(sm) + (uint32_t)SplitFwd<W, LOGQ, LE>::SMEM, st.phase);
         constexpr int PER = 16 / (int)sizeof(W);
 #pragma unroll
@@ -339,10 +346,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
             W av[PER];
             unpack16<W>(lds128(sm + tswz<W>(blk[q] * S + h)), av);
 #pragma unroll
-            for (int e = 0; e < PER; ++e) {
-              W prod = mont_redc_mul<W>(av[e], v[q * S + h + e], (W)pw.J, m.p);
-              v[q * S + h + e] = shoup_mul<W>(prod, (W)pw.K, (W)pw.Kp, m.p);
-            }
+            for (int e = 0; e < PER; ++e) v[q * S + h + e] = mont_redc_mul<W>(av[e], v[q * S + h + e], (W)pw.J, m.p);
           }
       } else {
 #pragma unroll
@@ -625,12 +629,13 @@ static cudaError_t run_split_k(void* x, size_t batch, const void* tw, uint64_t p
 }
 
 cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
-                          const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s) {
-  PwArgs pw{pw_a, pw_b, J, K, Kp};
+                          const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s,
+                          const void* tw1s) {
+  PwArgs pw{pw_a, pw_b, J, K, Kp, tw1s};
   // fused (pw_a set): inverse -- a <- InvNTT(a * b L^{-1}); forward -- a <- NTT(x) * a L^{-1}, x only
   // read (K = 2 only)
   const bool fused = pw_a != nullptr;
-  if (fused && !inverse && split_k() != 2) return cudaErrorNotSupported;
+  if (fused && !inverse && (split_k() != 2 || !tw1s)) return cudaErrorNotSupported;
   if (wbytes == 8) {
     if (logn != kContigMaxLog64 + 1) return cudaErrorInvalidValue;
     constexpr int L = kContigMaxLog64 + 1;

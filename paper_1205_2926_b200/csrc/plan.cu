@@ -61,10 +61,10 @@ bool is_prime_u64(uint64_t n) {
 
 // Table of (root^e, floor(root^e beta / p)) for e < count, interleaved pairs of
 // the plan's word width.
-std::vector<uint8_t> make_table(uint64_t p, uint64_t root, uint64_t count, unsigned bits) {
+std::vector<uint8_t> make_table(uint64_t p, uint64_t root, uint64_t count, unsigned bits, uint64_t scale = 1) {
   const size_t wb = bits / 8;
   std::vector<uint8_t> out(count * 2 * wb);
-  uint64_t w = 1 % p;
+  uint64_t w = scale % p;  // entries scale * root^e
   for (uint64_t e = 0; e < count; ++e) {
     const uint64_t wp = (uint64_t)(((u128)w << bits) / p);
     if (wb == 8) {
@@ -133,6 +133,7 @@ struct ntt_plan_s {
   std::vector<unsigned> passes;
   // device tables
   void* tw_fwd = nullptr;  // single pass: omega^e, e < L/2
+  void* tw1s = nullptr;    // cluster sizes: stage-1 entries omega^e K_scale, e < L/2 (fused convolution)
   void* tw_inv = nullptr;  // single pass: omega^{-e}
   std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables
   std::vector<void*> owned;
@@ -385,6 +386,11 @@ ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsig
                                                     : make_stage_table(p, omega, ell, bits),
                      &pl->tw_fwd)) != NTT_OK ||
         (st = upload(pl, make_stage_table(p, pl->omega_inv, ell, bits), &pl->tw_inv)) != NTT_OK) {
+      free_plan(pl);
+      return st;
+    }
+    if (nttb::split2_supported((int)pl->wbytes, (int)ell) &&
+        (st = upload(pl, make_table(p, omega, (uint64_t)1 << (ell - 1), bits, pl->K_scale), &pl->tw1s)) != NTT_OK) {
       free_plan(pl);
       return st;
     }
@@ -718,7 +724,7 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t pl, void* a, void* b, size_t batch, nt
     // a-hat; then the plain inverse of a.  b is only read.
     DeviceGuard g(pl->device);
     cudaError_t e = nttb::launch_split2((int)pl->wbytes, (int)pl->ell, false, b, batch, pl->tw_fwd, pl->p, a, b, pl->J,
-                                        pl->K_scale, pl->Kp_scale, (cudaStream_t)stream);
+                                        pl->K_scale, pl->Kp_scale, (cudaStream_t)stream, pl->tw1s);
     if (e != cudaErrorNotSupported) {
       if (e != cudaSuccess) return cuda_fail(e);
       st = ntt_inverse(pl, a, batch, stream);
