@@ -114,12 +114,21 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+try:  # the current stream's raw handle without building a torch.cuda.Stream object (~1 us per call)
+    import torch as _torch
+    _raw_stream = _torch._C._cuda_getCurrentRawStream
+    _cur_dev = _torch._C._cuda_getDevice
+except Exception:  # no torch build with CUDA: the legacy default stream
+    _raw_stream = _cur_dev = None
+
+
 def _stream(stream) -> int:
     if stream is None:
+        if _raw_stream is None:
+            return 0
         try:
-            import torch
-            return torch.cuda.current_stream().cuda_stream
-        except Exception:  # no torch / no device: legacy default stream
+            return _raw_stream(_cur_dev())
+        except Exception:  # no device: legacy default stream
             return 0
     if isinstance(stream, int):
         return stream

@@ -225,18 +225,32 @@ static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bo
       return run_tma<W, LOGN, INV, PLO1, BF, kTmaLatencyLE>(x, batch, tw, p, norm, s);
   }
   using Sh = TmaShape<W, LOGN, LE>;
-  auto enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
   const uint64_t rows = (uint64_t)batch * Sh::N / Sh::ROW_WORDS;
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)Sh::ROW_WORDS, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {(cuuint32_t)Sh::ROW_WORDS, (cuuint32_t)Sh::BOX_ROWS};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, x, dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  // The tensor map depends only on (x, rows) for this instantiation: the last one is reused, so a
+  // latency-bound caller (config C1, one transform per call) skips the host-side encode.
+  struct MapCache { const void* x = nullptr; uint64_t rows = 0; int dev = -1; CUtensorMap map; };
+  static thread_local MapCache mc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (mc.x != x || mc.rows != rows || mc.dev != dev) {
+    auto enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {(cuuint64_t)Sh::ROW_WORDS, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {(cuuint32_t)Sh::ROW_WORDS, (cuuint32_t)Sh::BOX_ROWS};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&mc.map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, x,
+                      dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+      mc.x = nullptr;
+      return cudaErrorInvalidValue;
+    }
+    mc.x = x;
+    mc.rows = rows;
+    mc.dev = dev;
+  }
+  const CUtensorMap& map = mc.map;
   auto kern = k_contig_tma<W, LOGN, LE, INV, PLO1, BF>;
   static int occ = 0;
   if (!occ) {
