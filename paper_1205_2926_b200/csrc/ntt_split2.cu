@@ -15,8 +15,9 @@
 //
 // Inverse (Algorithm 1 run backwards): stages ell..s+1 are K independent
 // Q-point inverses (one per CTA); stages s..1 (Algorithm 4, W = zeta_i^{-k}) act on
-// the K values at positions j + tQ, read from the K CTAs' shared memory through
-// distributed shared memory; CTA r finishes j in [rQ/K, (r+1)Q/K).  With PW the
+// the K values at positions j + tQ through distributed shared memory (K = 2: each CTA pushes the
+// half it does not finish into the other's shared memory; K = 4: reads from the K CTAs); CTA r
+// finishes j in [rQ/K, (r+1)Q/K).  With PW the
 // pointwise product c = a b L^{-1} is formed while loading, so a cyclic
 // convolution needs no separate pointwise pass.
 //
@@ -380,41 +381,63 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       }
     } else {
       // stages s..1 across the cluster through DSMEM (Algorithm 4)
+      constexpr int PER_CTA = Q / K;
+      if constexpr (K == 2) {
+        // Stage 1 across the pair, push model: thread t of either CTA holds positions j = hD + t of its
+        // block (D = T here), so the two values of butterfly j sit in the same thread of the two CTAs.
+        // Each CTA stores the half it does not finish straight from registers into the other's shared
+        // memory (16-byte-free remote stores: no DSMEM load latency), keeps the other half in
+        // registers, and after one cluster barrier finishes its half (CTA 0: h < S/2) with local loads.
+        static_assert(G == 1 && D == Sh::T, "one column of the block per thread");
+        constexpr int H2 = S / 2;
+        // the other CTA has consumed its round inputs (relaxed: this CTA's inputs are consumed too,
+        // the round's arithmetic used them) before this CTA's stores overwrite its buffer
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+        W* other = cluster.map_shared_rank(sm, rank ^ 1);
+        if (rank == 0) {
+#pragma unroll
+          for (int h = 0; h < H2; ++h) other[h * D + t] = v[H2 + h];
+        } else {
+#pragma unroll
+          for (int h = 0; h < H2; ++h) other[h * D + t] = v[h];
+        }
+        cluster.sync();  // the pushed halves are visible
+        const int off = stage_off(LOGL, 1);
+        constexpr int U = sizeof(W) == 4 ? 8 : 4;
+        static_assert(H2 % U == 0, "whole groups");
+        auto finish = [&](const W* mine_v, bool r0) {
+#pragma unroll
+          for (int h0 = 0; h0 < H2; h0 += U) {
+            W u0[U], u1[U], w[U], wp[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int j = (r0 ? 0 : PER_CTA) + (h0 + u) * D + t;
+              const W theirs = sm[(h0 + u) * D + t];
+              u0[u] = r0 ? mine_v[h0 + u] : theirs;  // x_j sits in CTA 0, x_{j+Q} in CTA 1
+              u1[u] = r0 ? theirs : mine_v[h0 + u];
+              ldtw<W>(tw_full, (uint32_t)(off + j), w[u], wp[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int j = (r0 ? 0 : PER_CTA) + (h0 + u) * D + t;
+              bfly_alg4<W, PLO1>(u0[u], u1[u], w[u], wp[u], m);
+              xb[j] = norm4<W>(u0[u], m.p, m.p2);
+              xb[j + Q] = norm4<W>(u1[u], m.p, m.p2);
+            }
+          }
+        };
+        if (rank == 0) finish(v, true);
+        else finish(v + H2, false);
+        // no trailing cluster barrier: the other CTA's next stores into this buffer come after the
+        // next transform's pre-store barrier, which this CTA reaches only after these loads
+      } else {
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
         for (int h = 0; h < S; ++h) sm[sswz<W>(h * D + c[q])] = v[q * S + h];
       cluster.sync();
-      constexpr int PER_CTA = Q / K;
-      if constexpr (K == 2) {  // (K = 4: the general loop below)
-        // stage 1 across the pair: this CTA finishes j in [rank Q/2, (rank+1) Q/2); its own block
-        // by LDS, the other's through DSMEM.  Groups of U positions with every load issued first,
-        // so the ~200-cycle DSMEM latency overlaps (it was the epilogue's main stall).
-        constexpr int UU = sizeof(W) == 4 ? 8 : 4, IT = PER_CTA / Sh::T, U = IT >= UU ? UU : IT;
-        const W* other = cluster.map_shared_rank(sm, rank ^ 1);
-        const int off = stage_off(LOGL, 1);
-#pragma unroll 1
-        for (int j0 = 0; j0 < IT; j0 += U) {
-          W u0[U], u1[U], w[U], wp[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = rank * PER_CTA + t + Sh::T * (j0 + u);
-            const W mine = sm[sswz<W>(j)], theirs = other[sswz<W>(j)];
-            u0[u] = rank == 0 ? mine : theirs;  // x_j sits in CTA 0, x_{j+Q} in CTA 1
-            u1[u] = rank == 0 ? theirs : mine;
-            ldtw<W>(tw_full, (uint32_t)(off + j), w[u], wp[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = rank * PER_CTA + t + Sh::T * (j0 + u);
-            bfly_alg4<W, PLO1>(u0[u], u1[u], w[u], wp[u], m);
-            xb[j] = norm4<W>(u0[u], m.p, m.p2);
-            xb[j + Q] = norm4<W>(u1[u], m.p, m.p2);
-          }
-        }
-        cluster_sync_war();  // the other CTA is done reading this CTA's shared memory
-      } else {
+      {
         const W* part[K];
 #pragma unroll
         for (int tt = 0; tt < K; ++tt) part[tt] = cluster.map_shared_rank(sm, tt);  // values at j + tt*Q
@@ -441,6 +464,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           for (int tt = 0; tt < K; ++tt) xb[j + tt * Q] = norm4<W>(u[tt], m.p, m.p2);
         }
         cluster_sync_war();  // the other CTAs are done reading this CTA's shared memory
+      }
       }
     }
   } else {
