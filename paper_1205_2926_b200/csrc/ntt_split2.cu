@@ -188,12 +188,7 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
         for (int kk = F::NX + F::NB; kk < F::NCH; ++kk) F::issue(st.map, st.b, kk, sbase);
     }
   }
-  // every chunk consumed: the X slots take the next transform's first chunks
-  fence_proxy_async_smem();
-  __syncthreads();
-  if (threadIdx.x == 0 && st.next_b < st.batch)
-#pragma unroll
-    for (int kk = 0; kk < F::NX; ++kk) F::issue(st.map, st.next_b, kk, sbase);
+  // (the X slots take the next transform's first chunks at the first round's exchange barrier)
 }
 
 
@@ -480,9 +475,18 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     constexpr bool FIRST_WL = INV && Sh::R >= 3 && warp_local_exchange<LOGQ, LE, Sh::R - 1, Sh::R - 2>();
     using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
     constexpr bool REFILL = INV && St::NX > 0 && (FIRST_WL ? r == Sh::R - 2 : first);
-    if constexpr (REFILL) fence_proxy_async_smem();
+    // forward (K = 2): the first round's exchange barrier also tells that stage 1 has consumed every
+    // staged chunk, so the spare slots take the next transform's first chunks there
+    constexpr bool FWD_REFILL = !INV && K == 2 && first;
+    if constexpr (REFILL || FWD_REFILL) fence_proxy_async_smem();
     if constexpr (WL) __syncwarp();
     else __syncthreads();
+    if constexpr (FWD_REFILL) {
+      using F = SplitFwd<W, LOGQ, LE>;
+      if (threadIdx.x == 0 && st.next_b < st.batch)
+#pragma unroll
+        for (int kk = 0; kk < F::NX; ++kk) F::issue(st.map, st.next_b, kk, smem_u32(sm));
+    }
     if constexpr (REFILL) {  // the spare slots take the next transform's chunks
       if (threadIdx.x == 0 && st.next_b < st.batch) St::issue(st.map, st.next_b, rank, 0, St::NX, smem_u32(sm));
     }
