@@ -255,8 +255,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           }
           v[q * S + h] = u[0];
         }
-      // every CTA has read x_b: in-place stores below are safe.  (Measured: the relaxed
-      // cluster_sync_war() here makes the forward 15-35% slower, so the full barrier stays.)
+      // every CTA has read x_b: in-place stores below are safe (K = 4 keeps one full barrier here;
+      // K = 2 splits it into an arrive after stage 1 and a wait before the store)
       cluster.sync();
     } else {
       // this CTA's block of the bit-reversed input (contiguous runs, from shared memory);
@@ -301,8 +301,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
           }
         }
       }
-      // no barrier needed here: the cross-CTA stores of the epilogue follow the
-      // epilogue's cluster barrier, after every CTA has loaded its block
+      // no barrier needed here: the epilogue's cross-CTA accesses follow its own cluster barrier,
+      // after every CTA has consumed its block
     }
   } else {
 #pragma unroll
