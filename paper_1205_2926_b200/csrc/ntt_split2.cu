@@ -50,6 +50,31 @@ template <class W> __device__ __forceinline__ int sswz(int i) {  // element XOR 
   return i ^ ((i >> S) & ((1 << S) - 1));
 }
 
+// Forward's last round with G > 1 groups of contiguous runs (u64 2^15: rounds 5,5,4): groups assigned
+// g = t G + q instead of g = t + T q give each thread E consecutive words, so a warp holds the same
+// 32 E words as in the previous round (G = 1, D <= 32) and their exchange is warp-local.  Its layout
+// then swaps 16-byte chunks by (row / 2) mod 8 (xswz) -- conflict-free for both sides, where the
+// element swizzle of the other exchanges is not.
+#ifndef NTT_SPLIT_REMAP
+#define NTT_SPLIT_REMAP 1
+#endif
+template <int LOGQ, int LE, int r> __host__ __device__ constexpr bool split_remap_last() {
+  using RC = Rounds<LOGQ, LE>;
+  constexpr int Q = 1 << LOGQ, E = 1 << LE, T = Q >> LE;
+  if constexpr (!NTT_SPLIT_REMAP || r != RC::R - 1 || r == 0) {
+    return false;
+  } else {
+    constexpr int S = 1 << RC::sr(r), D = Q >> (RC::level(r) + RC::sr(r));
+    constexpr int Sp = 1 << RC::sr(r - 1), Dp = Q >> (RC::level(r - 1) + RC::sr(r - 1));
+    return S < E && D == 1 && Sp == E && Dp <= 32 && 32 % Dp == 0 && T % 32 == 0;
+  }
+}
+template <class W> __device__ __forceinline__ int xswz(int i) {  // 16-byte chunk ^= (row / 2) mod 8
+  constexpr int CS = sizeof(W) == 8 ? 1 : 2;  // log2 words per chunk
+  constexpr int RS = sizeof(W) == 8 ? 4 : 5;  // log2 words per 128-byte row
+  return i ^ ((((i >> RS) >> 1) & 7) << CS);
+}
+
 template <int LOGQ, int LE, int K, int WB = 8> struct SplitShape {
   static constexpr int Q = 1 << LOGQ, E = 1 << LE, T = Q / E;
   static constexpr int S_SPLIT = K == 4 ? 2 : 1;  // log2 K
@@ -204,10 +229,11 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   constexpr int S = 1 << SR, G = Sh::E >> SR;
   constexpr int D = Q >> (LEVEL + SR), B = Q >> LEVEL;
   const TwPair<W>* tw_sub = tw_full + ((1 << LOGL) - Q);  // stages s+1..ell of the full per-stage table
+  constexpr bool REMAP = !INV && split_remap_last<LOGQ, LE, r>();  // this round: remapped groups
   int c[G], blk[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) {
-    const int g = t + Sh::T * q;
+    const int g = REMAP ? t * G + q : t + Sh::T * q;
     blk[q] = g / D;
     c[q] = g % D;
   }
@@ -308,7 +334,14 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
     for (int q = 0; q < G; ++q)
 #pragma unroll
-      for (int h = 0; h < S; ++h) v[q * S + h] = sm[sswz<W>(blk[q] * B + h * D + c[q])];
+      for (int h = 0; h < S; ++h) {
+        if constexpr (REMAP) {
+          constexpr int PER = 16 / (int)sizeof(W);
+          if (h % PER == 0) unpack16<W>(lds128(sm + xswz<W>(blk[q] * B + h)), v + q * S + h);
+        } else {
+          v[q * S + h] = sm[sswz<W>(blk[q] * B + h * D + c[q])];
+        }
+      }
   }
   if constexpr (PW && !INV && last) {
     // forward with the pointwise product: every thread has its last-round inputs, so the buffer
@@ -355,7 +388,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       constexpr int PER = 16 / (int)sizeof(W);
       // every thread has read its last-round inputs from sm (only its own warp's region when the
       // exchange into this round was warp-local and no a-hat was staged over the buffer)
-      if constexpr (!PW && warp_local_exchange<LOGQ, LE, r - 1, r>()) __syncwarp();
+      if constexpr (!PW && (REMAP || warp_local_exchange<LOGQ, LE, r - 1, r>())) __syncwarp();
       else __syncthreads();
 #pragma unroll
       for (int q = 0; q < G; ++q)
@@ -471,7 +504,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     // (rounds.cuh).  The inverse's spare-slot refill needs every thread past its first round (a CTA
     // barrier): it rides on the first exchange, or on the second when the first is warp-local.
     constexpr int nr_ = INV ? r - 1 : r + 1;
-    constexpr bool WL = warp_local_exchange<LOGQ, LE, r, nr_>() && !(INV && Sh::R < 3);
+    constexpr bool NEXT_REMAP = !INV && split_remap_last<LOGQ, LE, nr_>();  // writes into the remapped round
+    constexpr bool WL = (warp_local_exchange<LOGQ, LE, r, nr_>() || NEXT_REMAP) && !(INV && Sh::R < 3);
     constexpr bool FIRST_WL = INV && Sh::R >= 3 && warp_local_exchange<LOGQ, LE, Sh::R - 1, Sh::R - 2>();
     using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
     constexpr bool REFILL = INV && St::NX > 0 && (FIRST_WL ? r == Sh::R - 2 : first);
@@ -493,7 +527,10 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
     for (int q = 0; q < G; ++q)
 #pragma unroll
-      for (int h = 0; h < S; ++h) sm[sswz<W>(blk[q] * B + h * D + c[q])] = v[q * S + h];
+      for (int h = 0; h < S; ++h) {
+        const int i = blk[q] * B + h * D + c[q];
+        sm[NEXT_REMAP ? xswz<W>(i) : sswz<W>(i)] = v[q * S + h];
+      }
     if constexpr (WL) __syncwarp();
     else __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
