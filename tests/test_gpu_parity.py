@@ -406,6 +406,29 @@ def test_config3_exact_integer_product(ntt):
         assert (o[i, 2 * half - 1:, 0] == 0).all()
 
 
+@pytest.mark.parametrize("p,bits,ell,batch", [(P62, 64, 15, 1), (P62, 64, 15, 149), (P62G, 64, 15, 75),
+                                               (P30, 32, 16, 1), (P30, 32, 16, 149)])
+def test_cluster_sizes_ragged_batches(ntt, p, bits, ell, batch):
+    """The 2-CTA cluster kernel (k_splitk) over batches that are not whole waves of its 74 clusters (one
+    transform; two waves plus one): first, middle and last transforms whole against the oracle (forward),
+    every transform through inverse o forward = L x."""
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(batch * L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(4), batch, bound=p)
+    xh = x.cpu().numpy().astype(np.uint64).reshape(batch, L)
+    plan.forward(x)
+    fh = x.cpu().numpy().astype(np.uint64).reshape(batch, L)
+    picks = sorted({0, batch // 2, batch - 1})
+    ref = oracle.ntt_forward(p, w, xh[picks], nthreads=NTHREADS)
+    assert np.array_equal(fh[picks], ref)
+    plan.inverse(x)
+    got = x.cpu().numpy().astype(np.uint64).reshape(batch, L).astype(object)
+    assert np.array_equal(got, (xh.astype(object) * L) % p)
+
+
 @pytest.mark.parametrize("ell", [22, 24, 26])
 def test_u32_long_transforms(ntt, ell):
     """beta = 2^32 up to the longest length its primes allow (p = 469762049 = 7*2^26+1, so 2^26): the
