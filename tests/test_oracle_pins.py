@@ -319,3 +319,57 @@ def test_crt_gives_exact_integer_product():
                                                             oracle.ntt_forward(q, w, pb), scale_L=L)))
     got = oracle.crt(res, RNS3)
     assert got[:2 * half - 1] == [int(v) for v in exact] and got[2 * half - 1:] == [0] * (L - 2 * half + 1)
+
+
+# ---------------------------------------------------------------- poly_eval / ntt_output_at
+# orc_poly_eval (Horner) and its wrapper ntt_output_at are the oracle's route to sampled outputs of
+# long transforms (2^22-2^28, the C4 sample) in the GPU parity tests; pinned here against the direct
+# DFT (P:24 sum form), closed forms of the evaluation form ("evaluation at 1, omega, ...") and a
+# mutation control.
+@pytest.mark.parametrize("p", [P30, P62, 469762049])
+def test_output_at_equals_direct_dft(p):
+    """ntt_output_at(p, omega, a, j) = b_{rev(j)} of the O(L^2) direct sum, every j, L <= 2^10."""
+    rng = np.random.default_rng(p & 0xFFFF)
+    for ell in (0, 1, 2, 5, 10):
+        L = 1 << ell
+        w = root(p, L)
+        a = rng.integers(0, p, size=L, dtype=np.uint64)
+        b = oracle.dft_direct(p, w, a)
+        got = [oracle.ntt_output_at(p, w, a, j) for j in range(L)]
+        assert got == [int(b[bitrev(j, ell)]) for j in range(L)], (p, ell)
+
+
+def test_poly_eval_small_values():
+    """a(x) = 1 + 2x + 3x^2: a(5) = 86 = 8 mod 13; a(0) = a_0; a(1) = sum a_i; a(-1) alternating sum."""
+    assert oracle.poly_eval(13, [1, 2, 3], 5) == 8
+    assert oracle.poly_eval(13, [1, 2, 3], 0) == 1
+    assert oracle.poly_eval(P62, [P62 - 1, P62 - 1, 5], 1) == (2 * (P62 - 1) + 5) % P62
+    assert oracle.poly_eval(P62, [7, 11, 13, 17], P62 - 1) == (7 - 11 + 13 - 17) % P62
+    assert oracle.poly_eval(P30, [], 5) == 0
+
+
+@pytest.mark.parametrize("p", [P62, P30])
+def test_output_at_closed_forms_2p20(p):
+    """L = 2^20: shifted delta e_s gives omega^{s rev(j)}; all-ones gives L at j = 0 and 0 elsewhere."""
+    ell = 20
+    L = 1 << ell
+    w = root(p, L)
+    s = 987654
+    e = np.zeros(L, dtype=np.uint64)
+    e[s] = 1
+    ones = np.ones(L, dtype=np.uint64)
+    for j in [0, 1, L - 1] + random.Random(5).sample(range(L), 6):
+        assert oracle.ntt_output_at(p, w, e, j) == pow(w, s * bitrev(j, ell), p)
+        assert oracle.ntt_output_at(p, w, ones, j) == (L % p if j == 0 else 0)
+
+
+def test_output_at_mutation_control():
+    """A reversed coefficient order (a_{L-1-i}) must not reproduce the transform."""
+    p, ell = P62, 8
+    L = 1 << ell
+    w = root(p, L)
+    a = np.random.default_rng(9).integers(0, p, size=L, dtype=np.uint64)
+    b = oracle.dft_direct(p, w, a)
+    rev_a = a[::-1].copy()
+    mism = sum(oracle.ntt_output_at(p, w, rev_a, j) != int(b[bitrev(j, ell)]) for j in range(L))
+    assert mism > L // 2
