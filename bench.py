@@ -2,15 +2,22 @@
 """Benchmark of the batched NTT hot path (BASELINE.json metric: NTT butterflies/s and
 achieved HBM GB/s) on B200.
 
-Default workload = BASELINE.json configs[1] (config C2): 4096 transforms of L = 2^12 over
-p = 29*2^57+1 (beta = 2^64), one step = forward + inverse of the whole batch.  Other
-configs (--config c1..c5) are available for measurement; the driver runs the default.
+Default workload = BASELINE.json configs[3] (config C4), the largest configuration that fits one
+GPU: 64 transforms of L = 2^24 over p = 29*2^57+1 (beta = 2^64), one step = the forward
+transform of the whole batch (two kernel passes: a four-step column pass and the row pass).
+Other configs (--config c1..c5) are available for measurement; the driver runs the default.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl native|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl native|reference]
 
-N > 1: launched by torchrun, one rank per GPU over NCCL; each rank transforms its own
-4096-transform shard (weak scaling, no data-path collective), time = max over ranks.
-Prints ONE JSON line on rank 0.
+N > 1: launched by torchrun (or, when WORLD_SIZE is unset, bench.py re-launches itself through
+torch.distributed.run with N ranks; it exits non-zero if the box has fewer than N GPUs), one rank
+per GPU over NCCL.  C4's 64 transforms are split over the ranks (strong scaling, no data-path
+collective), time = max over ranks.  Prints ONE JSON line on rank 0.
+
+Roofline: for the dominant kernel, T_MUL = its nontrivial Shoup products
+((L/2) ell - (L-1) per transform over all passes, split per pass incl. the four-step twiddle
+multiplies) / the derived integer-pipe peak, T_HBM = its algorithmic bytes (one read + one
+write of the data per pass) / MEASURED_PEAKS.json hbm_gbs; frac = max(T_MUL, T_HBM) / measured.
 """
 from __future__ import annotations
 
@@ -69,6 +76,49 @@ def derived_alu_peak(bits, p, sms, clock_mhz):
     else:
         cyc = 8
     return sms * clock_mhz * 1e6 * 4 * 32 / cyc
+
+
+def nontrivial(ell):
+    """Nontrivial (W != 1) butterflies of one length-2^ell Algorithm 1 transform: (L/2) ell - (L-1)
+    (the L-1 butterflies with W = 1 need no multiply)."""
+    L = 1 << ell
+    return (L // 2) * ell - (L - 1) if ell else 0
+
+
+def pass_products(ell, passes, j, batch):
+    """Nontrivial Shoup products of kernel pass j of the schedule `passes` (outermost first) over
+    `batch` transforms.  Pass j views each block of B = 2^(ell - outer) words as N = 2^passes[j] rows
+    x S columns: S column NTTs of length N plus the four-step twiddles omega_B^{c rev(r)}, of which
+    (N-1)(S-1) are not 1 (r = 0 or c = 0 give W = 1); the last pass has S = 1 (row NTTs only).
+    Summed over the passes this is exactly batch * nontrivial(ell) (DESIGN.md Roofline)."""
+    outer = sum(passes[:j])
+    n = passes[j]
+    N, S = 1 << n, 1 << (ell - outer - n)
+    blocks = batch << outer
+    return blocks * (S * nontrivial(n) + (N - 1) * (S - 1))
+
+
+def per_rank_batch(cfg, world):
+    batch = cfg["batch"]
+    if cfg["scaling"] == "strong" and world > 1 and cfg["key"] != "c5":
+        assert batch % world == 0, "strong-scaled batch must divide over ranks"
+        batch //= world
+    return batch
+
+
+def config_dict(cfg, world):
+    """The `config` object of the JSON line; the native and the reference arm print the same one."""
+    L = 1 << cfg["ell"]
+    batch = per_rank_batch(cfg, world)
+    dist_c5 = cfg["key"] == "c5" and world > 1
+    bfly = butterflies(cfg, batch) // (world if dist_c5 else 1)
+    par = (f"four-step split over {world} GPUs (one all-to-all transpose)" if dist_c5
+           else f"batch-sharded x{world}, no collective")
+    big = batch * L * cfg["bits"] // 8 > (256 << 20)
+    return {"workload": cfg["workload"], "transforms_per_gpu": batch, "L": L, "butterflies_per_step_per_gpu": bfly,
+            "parallelism": par,
+            "l2": ("inputs larger than L2 (" + f"{batch * L * cfg['bits'] // 8 >> 20} MiB per GPU" + ") and "
+                   if big else "") + "L2 flushed between timed steps (256 MiB zero-fill, outside the step events)"}
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -191,10 +241,7 @@ def run_native(args, cfg, rank, world, local_rank):
     bits = cfg["bits"]
     dt = torch.uint64 if bits == 64 else torch.uint32
     wb = bits // 8
-    batch = cfg["batch"]
-    if cfg["scaling"] == "strong" and world > 1:
-        assert batch % world == 0, "strong-scaled batch must divide over ranks"
-        batch //= world
+    batch = per_rank_batch(cfg, world)
     plans = [ntt.Plan(p, root(p, L), cfg["ell"], bits, device=local_rank) for p in cfg["primes"]]
     conv = cfg["ops"] == ("conv",)
     dist_c5 = cfg["key"] == "c5" and world > 1  # one transform split four-step over the ranks
@@ -257,6 +304,15 @@ def run_native(args, cfg, rank, world, local_rank):
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream.synchronize()
 
+    info0 = plans[0].info()
+    n_pass = info0.n_passes
+    sched = [info0.pass_log2[i] for i in range(n_pass)]
+
+    def pass_name(op, j):
+        if n_pass == 1:
+            return f"{op} (single pass, 2^{cfg['ell']})"
+        return f"{op} pass {j} ({'row' if j == n_pass - 1 else 'column'} pass, 2^{sched[j]})"
+
     def step(evs=None):
         """One step: the whole hot path over this rank's batch.  evs: events between launches."""
         launches = 0
@@ -283,12 +339,16 @@ def run_native(args, cfg, rank, world, local_rank):
                     evs.append(("conv", torch.cuda.Event(enable_timing=True)))
                     evs[-1][1].record(stream)
         else:
+            # the plan's kernel passes one by one (ntt_transform_pass; in this order exactly
+            # ntt_forward / ntt_inverse), so each kernel is timed on its own
             for op in cfg["ops"]:
-                (plans[0].forward if op == "fwd" else plans[0].inverse)(x, stream=stream)
-                launches += ntt.last_launch_count()
-                if evs is not None:
-                    evs.append((op, torch.cuda.Event(enable_timing=True)))
-                    evs[-1][1].record(stream)
+                inv = op == "inv"
+                for j in (reversed(range(n_pass)) if inv else range(n_pass)):
+                    plans[0].transform_pass(x, j, inverse=inv, stream=stream)
+                    launches += ntt.last_launch_count()
+                    if evs is not None:
+                        evs.append((pass_name(op, j), torch.cuda.Event(enable_timing=True)))
+                        evs[-1][1].record(stream)
         return launches
 
     def reset_inputs():
@@ -362,49 +422,76 @@ def run_native(args, cfg, rank, world, local_rank):
     bfly_rank = butterflies(cfg, batch) // (world if dist_c5 else 1)
     value = bfly_rank * world * args.steps / (total_ms * 1e-3)
 
-    # ---- dominant kernel (largest share of the step) and its roofline
-    share = {k: sum(v) for k, v in kernel_ms.items()}
-    dom = max(share, key=share.get)
-    dom_ms = statistics.mean(kernel_ms[dom])
-    per_launch_bfly = butterflies(cfg, batch) // (len(plans) if conv else len(cfg["ops"]))
+    # ---- wk of every timed launch group: nontrivial Shoup products and algorithmic HBM bytes
+    # (one read + one write of the data per kernel pass)
+    wk = {}
+    data_bytes = batch * L * wb
     if dist_c5:
-        per_launch_bfly = bfly_rank
-    if conv:
-        per_launch_bfly = butterflies(cfg, batch) // len(plans)  # one cyclic convolution (3 NTTs) per prime
-    passes = plans[0].info().n_passes
-    # algorithmic HBM bytes per launch: one read + one write of the data per pass
-    if conv:
-        alg_bytes = (2 * batch * L * wb) * (2 * passes) + 3 * batch * L * wb + 2 * batch * L * wb * passes
+        ell1 = cfg["ell"] // 2
+        ell2 = cfg["ell"] - ell1
+        n1, n2 = 1 << ell1, 1 << ell2
+        ncol = -(-ell1 // (9 if bits == 64 else 10))  # column passes of <= kColsMax stages
+        cols_w = ((n2 // world) * nontrivial(ell1) + (n1 - 1) * (n2 // world), 2 * ncol * (L // world) * wb)
+        wk = {"cols": cols_w, "cols+p2p_exchange": cols_w, "all_to_all": (0, 2 * (L // world) * wb),
+                "rows": ((n1 // world) * nontrivial(ell2), 2 * (L // world) * wb)}
+    elif conv:
+        # forward(a), forward(b) with the pointwise product fused, inverse: 3 transforms + L products,
+        # bytes: a read+write, b read + a-hat read + c-hat write, c read+write
+        wk = {"conv": (3 * batch * nontrivial(cfg["ell"]) + batch * L, 7 * data_bytes)}
     else:
-        alg_bytes = 2 * batch * L * wb * passes
-    achieved_bfly = per_launch_bfly / (dom_ms * 1e-3)
+        for op in cfg["ops"]:
+            for j in range(n_pass):
+                wk[pass_name(op, j)] = (pass_products(cfg["ell"], sched, j, batch), 2 * data_bytes)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "B200_PROFILING.md (of fallback)"
+
+    # ---- dominant kernel (largest share of the step) and its roofline
+    share = {k: sum(v) for k, v in kernel_ms.items()}
+    dom = max(share, key=share.get)
+    dom_ms = statistics.mean(kernel_ms[dom])
+    mults, alg_bytes = wk[dom]
+    t_mul = mults / alu_peak * 1e3
+    t_hbm = alg_bytes / (hbm_peak * 1e9) * 1e3
+    frac_int, frac_hbm = t_mul / dom_ms, t_hbm / dom_ms
+    alu_bound = t_mul >= t_hbm
+    # whole step: the same bounds summed over every launch group of the step
+    per_step = {k: len(v) / args.steps for k, v in kernel_ms.items()}
+    st_mul = sum(wk[k][0] * n for k, n in per_step.items()) / alu_peak * 1e3
+    st_hbm = sum(wk[k][1] * n for k, n in per_step.items()) / (hbm_peak * 1e9) * 1e3
+    step_mean = total_ms / args.steps
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+        entry = prof.get(args.config, {})
+        traffic = entry.get(dom, entry).get("dram_bytes_per_launch") if isinstance(entry.get(dom, entry), dict) else None
     except Exception:
         pass
     roofline = {
-        "bound": "alu",
-        "kernel": f"{dom} ({'fused single-pass' if passes == 1 else f'{passes}-pass four-step'})",
-        "achieved": round(achieved_bfly / 1e9, 2),
-        "peak": round(alu_peak / 1e9, 2),
-        "unit": "Gbutterflies/s",
-        "frac": round(achieved_bfly / alu_peak, 4),
-        "peak_source": (f"derived fmaheavy-pipe bound of Alg.3's multiplies at {sms} SMs x {clock_max:.0f} MHz "
-                        "(DESIGN.md Roofline)"),
+        "bound": "alu" if alu_bound else "hbm",
+        "kernel": dom + (" [3 launches: fwd(a), fwd(b)+pointwise, inv]" if conv else ""),
+        "achieved": round((mults / (dom_ms * 1e-3) / 1e9) if alu_bound else (alg_bytes / (dom_ms * 1e-3) / 1e9), 2),
+        "peak": round(alu_peak / 1e9, 2) if alu_bound else hbm_peak,
+        "unit": "G nontrivial Shoup products/s" if alu_bound else "GB/s",
+        "frac": round(max(frac_int, frac_hbm), 4),
+        "frac_int": round(frac_int, 4),
+        "frac_hbm": round(frac_hbm, 4),
+        "T_MUL_ms": round(t_mul, 4), "T_HBM_ms": round(t_hbm, 4), "measured_ms": round(dom_ms, 4),
+        "nontrivial_products_per_launch": mults,
+        "algorithmic_bytes_per_launch": alg_bytes,
+        "peak_source": (f"derived fmaheavy-pipe bound of one Alg. 3 Shoup product at {sms} SMs x {clock_max:.0f} MHz "
+                        f"(DESIGN.md Roofline); HBM {hbm_peak} GB/s from {hbm_src}"),
         "calibrated_register_only_Gbfly_s": round(calib_peak / 1e9, 2),
         "traffic": traffic,
         "hbm": {"achieved_GBps": round(alg_bytes / (dom_ms * 1e-3) / 1e9, 1), "peak_GBps": hbm_peak,
-                "frac": round(alg_bytes / (dom_ms * 1e-3) / 1e9 / hbm_peak, 4),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-                "algorithmic_bytes_per_launch": alg_bytes},
+                "frac": round(frac_hbm, 4), "peak_source": hbm_src},
+        "step": {"T_MUL_ms": round(st_mul, 4), "T_HBM_ms": round(st_hbm, 4), "measured_ms": round(step_mean, 4),
+                 "frac": round(max(st_mul, st_hbm) / step_mean, 4),
+                 "frac_int": round(st_mul / step_mean, 4), "frac_hbm": round(st_hbm / step_mean, 4)},
     }
 
     # ---- e2e: the same step through the C-ABI host-buffer call (ntt_execute_host),
@@ -500,16 +587,12 @@ def run_native(args, cfg, rank, world, local_rank):
             "scaling": "strong" if dist_c5 else cfg["scaling"], "vs_baseline": None,
             "dtype": "u64" if bits == 64 else "u32",
             "data": "synthetic: seeded counter-based uniform residues generated in HBM (synth/ definition)",
-            "config": {"workload": cfg["workload"], "transforms_per_gpu": batch, "L": L,
-                       "butterflies_per_step_per_gpu": bfly_rank,
-                       "parallelism": ((f"four-step split over {world} GPUs, all-to-all fused into the column pass "
-                                        "(P2P stores over NVLink, symmetric memory)" if exchange == "p2p" else
-                                        f"four-step split over {world} GPUs, one NCCL all_to_all") if dist_c5
-                                       else f"batch-sharded x{world}, no collective"),
-                       "passes": passes,
-                       "l2": "flushed between timed steps (256 MiB zero-fill, outside the step events)"},
-            "hbm_GBps": round(2 * batch * L * wb * passes * (len(cfg['ops']) if not conv else 3 * len(plans))
-                              * world * args.steps / (total_ms * 1e-3) / 1e9, 1),
+            "config": config_dict(cfg, world),
+            "passes": sched if not dist_c5 else None,
+            "exchange": (("all-to-all fused into the column pass (P2P stores over NVLink, symmetric memory)"
+                          if exchange == "p2p" else "one NCCL all_to_all_single") if dist_c5 else None),
+            "hbm_GBps": round(sum(wk[k][1] * len(v) for k, v in kernel_ms.items()) * world
+                              / (total_ms * 1e-3) / 1e9, 1),
             "roofline": roofline,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -586,7 +669,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -594,8 +677,27 @@ def main():
         args.warmup = 3
     cfg = dict(CONFIGS[args.config], key=args.config)
 
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus < 1:
+        sys.exit(f"bench.py: --gpus must be >= 1 (got {args.gpus})")
+    if env_world is not None and int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} does not match WORLD_SIZE={env_world}")
+    if env_world is None and args.gpus > 1 and args.impl == "native":
+        # one process per GPU: re-launch this command under torch.distributed.run with N ranks
+        import socket
+        import torch
+        n_dev = torch.cuda.device_count()
+        if n_dev < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but only {n_dev} CUDA device(s) are visible")
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
+    # the reference arm (CPU oracle) runs on rank 0 alone, also when --gpus N is given without torchrun
+    world = int(env_world) if env_world is not None else args.gpus
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     nthreads = len(os.sched_getaffinity(0))
 
@@ -607,9 +709,10 @@ def main():
         value, sample, sec = run_oracle_steps(cfg, args.steps, args.warmup, nthreads)
         out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "butterflies/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-               "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "u64" if cfg["bits"] == 64 else "u32",
+               "scaling": "strong" if (cfg["key"] == "c5" and world > 1) else cfg["scaling"], "vs_baseline": None,
+               "dtype": "u64" if cfg["bits"] == 64 else "u32",
                "data": "synthetic: seeded counter-based uniform residues (synth/ definition)",
-               "config": {"workload": cfg["workload"]},
+               "config": config_dict(cfg, world),
                "cpu_baseline": {"value": value, "unit": "butterflies/s", "cores": nthreads, "kind": "oracle",
                                 "sample": sample, "cpu": cpu_model()},
                "e2e": {"value": value, "unit": "butterflies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -103,6 +103,20 @@ ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stre
  * order, UNSCALED (ntt_inverse(ntt_forward(a)) = L*a mod p), normalised to [0,p). */
 ntt_status ntt_inverse(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream);
 
+/* One kernel pass of the plan's schedule (ntt_plan_info_t.pass_log2, outermost first), so a
+ * caller can time or interleave the passes of a multi-pass transform.  Running passes
+ * 0, 1, ..., n_passes-1 with inverse = 0 is exactly ntt_forward; running n_passes-1, ..., 0
+ * with inverse = 1 is exactly ntt_inverse (each in that order, on the same x; other orders
+ * are undefined).  Forward pass j < n_passes-1 is a four-step column pass (Algorithm 1's
+ * stages re-associated; four-step twiddle fused), the last one the
+ * contiguous row pass with the normalisation; the inverse mirrors it.
+ * Single-pass plans have one pass (0).  Same buffer contract and input ranges as
+ * ntt_forward / ntt_inverse (before the first pass); intermediate buffers hold redundant
+ * representatives (< 2p forward, < 4p inverse).  No range-checking mode here.
+ * NTT_ERR_ARG for pass >= n_passes or inverse > 1. */
+ntt_status ntt_transform_pass(ntt_plan_t plan, void* x, size_t batch, unsigned inverse, unsigned pass,
+                              ntt_stream_t stream);
+
 /* Pointwise product for the convolution use: c_k = a_k b_k [* L^{-1}]
  * mod p for k < batch*L.  Inputs in [0,2p); output canonical [0,p).  c may
  * alias a or b. */
@@ -124,7 +138,9 @@ ntt_status ntt_cyclic_convolve(ntt_plan_t plan, void* a, void* b, size_t batch, 
  * dev_buf_bytes >= L*word_bytes: the batch is streamed through it in chunks,
  * each chunk's H2D copy, transform(s) and D2H copy pipelined over the plan's own
  * streams so copies overlap compute.  Ordered after prior work on `stream`;
- * later work on `stream` waits for the whole call. */
+ * later work on `stream` waits for the whole call.  Thread safety: concurrent
+ * calls on one plan are serialised (each enqueues its whole pipeline under the
+ * plan's lock, on the plan's pipeline streams); they must use distinct dev_buf. */
 #define NTT_OP_FORWARD 1u
 #define NTT_OP_INVERSE 2u
 ntt_status ntt_execute_host(ntt_plan_t plan, unsigned ops, const void* host_in, void* host_out, size_t batch,

@@ -55,6 +55,7 @@ def _load() -> ctypes.CDLL:
         "ntt_plan_info": [vp, ctypes.POINTER(PlanInfo)],
         "ntt_forward": [vp, vp, sz, vp],
         "ntt_inverse": [vp, vp, sz, vp],
+        "ntt_transform_pass": [vp, vp, sz, uint, uint, vp],
         "ntt_pointwise_mul": [vp, vp, vp, vp, sz, uint, vp],
         "ntt_cyclic_convolve": [vp, vp, vp, sz, vp],
         "ntt_plan_twiddles": [vp, vp, vp],
@@ -88,7 +89,7 @@ def _load() -> ctypes.CDLL:
 _lib = _load()
 
 EXPORTED = (
-    "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_pointwise_mul",
+    "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_transform_pass", "ntt_pointwise_mul",
     "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
     "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p",
     "ntt_fourstep_rows_inv_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
@@ -191,6 +192,13 @@ class Plan:
 
     def inverse(self, x, batch=None, stream=None):
         _check(_lib.ntt_inverse(self._h, _ptr(x), self._batch(x, batch), _stream(stream)), "ntt_inverse")
+        return x
+
+    def transform_pass(self, x, pass_index, inverse=False, batch=None, stream=None):
+        """One kernel pass of the schedule (ntt_transform_pass): forward passes 0..n-1 in order
+        equal forward(); inverse passes n-1..0 in order equal inverse()."""
+        _check(_lib.ntt_transform_pass(self._h, _ptr(x), self._batch(x, batch), 1 if inverse else 0, pass_index,
+                                       _stream(stream)), "ntt_transform_pass")
         return x
 
     def pointwise_mul(self, c, a, b, batch=None, scale_inv_L=False, stream=None):

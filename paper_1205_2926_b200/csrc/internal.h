@@ -1,11 +1,31 @@
 // internal.h -- declarations shared by the host plan code (plan.cu) and the
 // kernel launchers (ntt_kernels.cu).  Not part of the public ABI.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace nttb {
+
+// A launch-configuration value (SM count, occupancy) cached per CUDA device: computed on the first
+// use on each device (cudaFuncSetAttribute and the occupancy queries are per device), read with
+// relaxed atomics so concurrent callers are safe (a concurrent first use computes it twice, with
+// the same result).  Devices beyond kMaxDevices are not cached.
+struct PerDevice {
+  static constexpr int kMaxDevices = 64;
+  std::atomic<int> v[kMaxDevices];
+  template <class F> int get(F compute) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) return compute();
+    int x = v[d].load(std::memory_order_relaxed);
+    if (!x) {
+      x = compute();
+      v[d].store(x, std::memory_order_relaxed);
+    }
+    return x;
+  }
+};
 
 // Limits of the on-chip (single-pass) transform and of the column pass, as
 // log2 of the sub-transform length, per word size.

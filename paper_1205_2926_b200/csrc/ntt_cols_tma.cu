@@ -197,6 +197,9 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
         *reinterpret_cast<uint4*>(dst) = val;
       }
       fence_proxy_async_smem();  // these generic reads precede the buffer's next TMA load
+      // with one round (R == 1) the next iteration's prefetch into this buffer is issued at the top of
+      // the loop, not behind a round's CTA barrier: every warp must have finished reading it first
+      if constexpr (Sh::R == 1) __syncthreads();
     } else if (threadIdx.x == 0) {
       const int bq = (int)(tile >> prm.log_colgroups), c0 = (int)(tile & cg_mask) * Sh::C;
 #pragma unroll
@@ -238,12 +241,13 @@ static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTable
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, FACT>;
-  static int occ = 0;
-  if (!occ) {
+  static PerDevice occ_cache;
+  const int occ = occ_cache.get([&] {
+    int o = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Sh::THREADS, Sh::SMEM);
-    if (occ <= 0) occ = 1;
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Sh::THREADS, Sh::SMEM);
+    return o > 0 ? o : 1;
+  });
   const uint64_t maxg = (uint64_t)occ * sm_count();
   const unsigned grid = (unsigned)(prm.n_tiles < maxg ? prm.n_tiles : maxg);
   if (!grid) return cudaSuccess;

@@ -252,12 +252,13 @@ static cudaError_t run_tma(void* x, size_t batch, const void* tw, uint64_t p, bo
   }
   const CUtensorMap& map = mc.map;
   auto kern = k_contig_tma<W, LOGN, LE, INV, PLO1, BF>;
-  static int occ = 0;
-  if (!occ) {
+  static PerDevice occ_cache;
+  const int occ = occ_cache.get([&] {
+    int o = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Sh::THREADS, Sh::SMEM);
-    if (occ <= 0) occ = 1;
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Sh::THREADS, Sh::SMEM);
+    return o > 0 ? o : 1;
+  });
   const size_t ntiles = (batch + Sh::K - 1) / Sh::K;
   const size_t maxg = (size_t)occ * sm_count();
   const unsigned grid = (unsigned)(ntiles < maxg ? ntiles : maxg);

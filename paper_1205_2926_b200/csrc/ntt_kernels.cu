@@ -366,15 +366,14 @@ __global__ void __launch_bounds__(256) k_calib(W* sink, W p, W w, W wp, unsigned
 }
 
 // ----------------------------------------------------------------- launch plumbing
-static int g_num_sms = 0;
 static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
+  static PerDevice cache;
+  return cache.get([] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  });
 }
 
 template <class KernelT> static int occupancy(KernelT k, int threads, size_t smem) {
@@ -397,8 +396,8 @@ static cudaError_t run_contig(void* x, size_t batch, const void* tw, uint64_t p,
   using Sh = ContigShape<LOGN, LE>;
   const size_t smem = Sh::R > 1 ? (size_t)Sh::K * Sh::N * sizeof(W) : 0;
   auto kern = k_contig<W, LOGN, LE, INV, GATHER, PLO1>;
-  static int occ = 0;
-  if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
+  static PerDevice occ_cache;
+  const int occ = occ_cache.get([&] { return occupancy(kern, Sh::THREADS, smem); });
   const size_t iters = (batch + Sh::K - 1) / Sh::K;
   const size_t maxg = (size_t)occ * num_sms();
   const unsigned grid = (unsigned)(iters < maxg ? iters : maxg);
@@ -418,8 +417,8 @@ static cudaError_t run_cols(void* x, const ColsParams& prm, const DevTables& t, 
   using Sh = ColsShape<W, LOGN, LE>;
   const size_t smem = (size_t)Sh::N * Sh::C * sizeof(W);
   auto kern = k_cols<W, LOGN, LE, INV, PLO1>;
-  static int occ = 0;
-  if (!occ) occ = occupancy(kern, Sh::THREADS, smem);
+  static PerDevice occ_cache;
+  const int occ = occ_cache.get([&] { return occupancy(kern, Sh::THREADS, smem); });
   const uint64_t maxg = (uint64_t)occ * num_sms();
   const unsigned grid = (unsigned)(prm.n_tiles < maxg ? prm.n_tiles : maxg);
   if (!grid) return cudaSuccess;

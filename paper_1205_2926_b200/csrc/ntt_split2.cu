@@ -644,8 +644,9 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
   attr[0].val.clusterDim.x = K;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  static int max_clusters = 0;
-  if (!max_clusters) {
+  static PerDevice mc_cache;
+  const int max_clusters = mc_cache.get([&] {
+    int mc = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t q = {};
     q.gridDim = dim3(K * 1024);
@@ -653,11 +654,12 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
     q.dynamicSmemBytes = smem;
     q.attrs = attr;
     q.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &q) != cudaSuccess || max_clusters <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc <= 0) {
       cudaGetLastError();
-      max_clusters = 148 / K;
+      mc = sm_count() / K;
     }
-  }
+    return mc;
+  });
   const size_t groups = batch < (size_t)max_clusters ? batch : (size_t)max_clusters;
   if (!groups) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};

@@ -148,6 +148,7 @@ struct ntt_plan_s {
   static constexpr int kRing = 8;           // max device buffers in the host pipeline's ring
   static constexpr int kDefaultRing = 4;
   static constexpr int kDefaultChunks = 8;
+  std::mutex host_mu;                        // held for a whole ntt_execute_host call (streams, ring events)
   cudaStream_t pipe[3] = {};                 // H2D, compute, D2H
   cudaEvent_t pipe_done[3] = {};
   cudaEvent_t ring_ev[3 * kRing] = {};       // loaded / computed / freed per ring buffer
@@ -503,12 +504,61 @@ static ntt_status check_range(ntt_plan_t pl, const void* x, size_t n, uint64_t b
   return h ? NTT_ERR_RANGE : NTT_OK;
 }
 
-static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
-  t_launches = 0;
+// One kernel pass of the schedule (no argument checks; callers validate).  Pass j indexes the
+// schedule outermost first: forward runs j = 0 .. np-1 (column passes, then the contiguous row pass,
+// which normalises), the inverse j = np-1 .. 0 (row pass first, the j = 0 column pass normalises).
+static cudaError_t run_pass(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse, unsigned j) {
+  const uint64_t L = (uint64_t)1 << pl->ell;
+  const unsigned np = (unsigned)pl->passes.size();
+  if (pl->ell == 0)  // identity; only the normalisation remains
+    return nttb::launch_normalize(pl->wbytes, x, batch, pl->p, inverse ? 1 : 0, s);
+  if (pl->bfly != NTT_BFLY_ALG3 && !inverse)  // F1/F2 ablation: on-chip TMA kernel only
+    return nttb::launch_contig_tma(pl->wbytes, (int)pl->ell, false, true, x, batch, pl->tw_fwd, pl->p, s,
+                                   (int)pl->bfly);
+  if (np == 1)
+    return launch_contig_any(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
+                             pl->p, s);
+  if (j + 1 == np) {  // contiguous row pass
+    const size_t rows = batch * (L >> pl->passes[np - 1]);
+    return launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], inverse, !inverse, x, rows,
+                             inverse ? pl->sub_inv[np - 1] : pl->sub_fwd[np - 1], pl->p, s);
+  }
+  // column pass j of the nested four-step
+  const unsigned C = 128 / pl->wbytes;
+  nttb::ColsParams prm{};
+  unsigned outer = 0;
+  for (unsigned i = 0; i < j; ++i) outer += pl->passes[i];
+  const unsigned logB = pl->ell - outer, logN = pl->passes[j], logS = logB - logN;
+  unsigned logC = 0;
+  while ((1u << logC) < C) ++logC;
+  prm.log_S = logS;
+  prm.log_colgroups = logS - logC;
+  prm.n_tiles = ((uint64_t)batch << outer) << prm.log_colgroups;
+  // per-level tables: exponent e = c rev(r) of omega_B, B = 2^logB (log_tw_mul = 0, ell = logB)
+  prm.log_tw_mul = 0;
+  prm.ell = logB;
+  prm.twiddle = 1;
+  prm.normalize = (inverse && j == 0) ? 1 : 0;
+  ntt_plan_s::FsTables t{};
+  if (fourstep_level_tables(pl, prm.ell, &t) != NTT_OK)  // built at plan creation: a cache hit
+    return cudaErrorMemoryAllocation;
+  prm.H = t.H;
+  nttb::DevTables tb{pl->sub_fwd[j], pl->sub_inv[j], t.fa, t.fb};
+  return launch_cols_any(pl->wbytes, (int)pl->passes[j], inverse, x, prm, tb, pl->p, s);
+}
+
+static ntt_status check_transform_args(ntt_plan_t pl, void* x, size_t batch) {
   if (!pl || (!x && batch) || (x && !aligned16(x))) return NTT_ERR_ARG;
-  if (!batch) return NTT_OK;
   const uint64_t L = (uint64_t)1 << pl->ell;
   if (batch > (SIZE_MAX / pl->wbytes) / L) return NTT_ERR_ARG;
+  return NTT_OK;
+}
+
+static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s, bool inverse) {
+  t_launches = 0;
+  if (ntt_status st = check_transform_args(pl, x, batch); st != NTT_OK) return st;
+  if (!batch) return NTT_OK;
+  const uint64_t L = (uint64_t)1 << pl->ell;
   DeviceGuard g(pl->device);
   if (!g.ok) return cuda_fail(cudaGetLastError());
   if (g_range_checks.load(std::memory_order_relaxed)) {
@@ -517,81 +567,15 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     ntt_status st = check_range(pl, x, batch * L, bound, s);
     if (st != NTT_OK) return st;
   }
+  const unsigned np = (pl->ell == 0 || (pl->bfly != NTT_BFLY_ALG3 && !inverse)) ? 1u : (unsigned)pl->passes.size();
+  if (np > 1 && pl->bfly != NTT_BFLY_ALG3 && !inverse) return NTT_ERR_UNSUPPORTED;
+  if (pl->bfly != NTT_BFLY_ALG3 && !inverse && !nttb::tma_supported((int)pl->wbytes, (int)pl->ell))
+    return NTT_ERR_UNSUPPORTED;
   cudaError_t e = cudaSuccess;
-  const unsigned np = (unsigned)pl->passes.size();
-  if (pl->ell == 0) {  // identity; only the normalisation remains
-    e = nttb::launch_normalize(pl->wbytes, x, batch, pl->p, inverse ? 1 : 0, s);
+  for (unsigned k = 0; k < np && e == cudaSuccess; ++k) {
+    e = run_pass(pl, x, batch, s, inverse, inverse ? np - 1 - k : k);
     ++t_launches;
-    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
   }
-  if (pl->bfly != NTT_BFLY_ALG3 && !inverse) {  // F1/F2 ablation: on-chip TMA kernel only
-    if (np != 1 || !nttb::tma_supported((int)pl->wbytes, (int)pl->ell)) return NTT_ERR_UNSUPPORTED;
-    e = nttb::launch_contig_tma(pl->wbytes, (int)pl->ell, false, true, x, batch, pl->tw_fwd, pl->p, s, (int)pl->bfly);
-    ++t_launches;
-    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
-  }
-  if (np == 1) {
-    e = launch_contig_any(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
-                          pl->p, s);
-    ++t_launches;
-    return e == cudaSuccess ? NTT_OK : cuda_fail(e);
-  }
-  // nested four-step: passes 0..np-2 are column passes, np-1 the contiguous row pass
-  const unsigned C = 128 / pl->wbytes;
-  auto cols_params = [&](unsigned j, bool normalize) {
-    nttb::ColsParams prm{};
-    unsigned outer = 0;
-    for (unsigned i = 0; i < j; ++i) outer += pl->passes[i];
-    const unsigned logB = pl->ell - outer, logN = pl->passes[j], logS = logB - logN;
-    unsigned logC = 0;
-    while ((1u << logC) < C) ++logC;
-    prm.log_S = logS;
-    prm.log_colgroups = logS - logC;
-    prm.n_tiles = ((uint64_t)batch << outer) << prm.log_colgroups;
-    // per-level tables: exponent e = c rev(r) of omega_B, B = 2^logB (log_tw_mul = 0, ell = logB)
-    prm.log_tw_mul = 0;
-    prm.ell = logB;
-    prm.twiddle = 1;
-    prm.normalize = normalize ? 1 : 0;
-    return prm;
-  };
-  auto level_tables = [&](unsigned j, nttb::ColsParams& prm, const void** fa, const void** fb) {
-    ntt_plan_s::FsTables t{};
-    const ntt_status st = fourstep_level_tables(pl, prm.ell, &t);  // built at plan creation: a cache hit
-    prm.H = t.H;
-    *fa = t.fa;
-    *fb = t.fb;
-    (void)j;
-    return st;
-  };
-  if (!inverse) {
-    for (unsigned j = 0; j + 1 < np && e == cudaSuccess; ++j) {
-      nttb::ColsParams prm = cols_params(j, false);
-      const void *fa = nullptr, *fb = nullptr;
-      if (ntt_status st = level_tables(j, prm, &fa, &fb); st != NTT_OK) return st;
-      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], fa, fb};
-      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], false, x, prm, t, pl->p, s);
-      ++t_launches;
-    }
-    if (e == cudaSuccess) {
-      const size_t rows = batch * (L >> pl->passes[np - 1]);
-      e = launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], false, true, x, rows, pl->sub_fwd[np - 1], pl->p, s);
-      ++t_launches;
-    }
-  } else {
-    const size_t rows = batch * (L >> pl->passes[np - 1]);
-    e = launch_contig_any(pl->wbytes, (int)pl->passes[np - 1], true, false, x, rows, pl->sub_inv[np - 1], pl->p, s);
-    ++t_launches;
-    for (int j = (int)np - 2; j >= 0 && e == cudaSuccess; --j) {
-      nttb::ColsParams prm = cols_params((unsigned)j, j == 0);
-      const void *fa = nullptr, *fb = nullptr;
-      if (ntt_status st = level_tables((unsigned)j, prm, &fa, &fb); st != NTT_OK) return st;
-      nttb::DevTables t{pl->sub_fwd[j], pl->sub_inv[j], fa, fb};
-      e = launch_cols_any(pl->wbytes, (int)pl->passes[j], true, x, prm, t, pl->p, s);
-      ++t_launches;
-    }
-  }
-  (void)C;
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 
@@ -610,6 +594,10 @@ ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, vo
   if (batch > SIZE_MAX / tbytes || dev_buf_bytes < tbytes) return NTT_ERR_ARG;
   DeviceGuard g(pl->device);
   using P = ntt_plan_s;
+  // the pipeline streams and the ring events are per plan: one call enqueues at a time, so a
+  // concurrent call on another thread waits (its copies would otherwise interleave with this
+  // call's event records); the work itself is ordered through the shared pipeline streams
+  std::lock_guard<std::mutex> call_lk(pl->host_mu);
   {
     std::lock_guard<std::mutex> lk(pl->mu);
     if (!pl->start_ev) {
@@ -694,6 +682,20 @@ ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stre
 
 ntt_status ntt_inverse(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream) {
   return run_transform(plan, x, batch, (cudaStream_t)stream, true);
+}
+
+ntt_status ntt_transform_pass(ntt_plan_t pl, void* x, size_t batch, unsigned inverse, unsigned pass,
+                              ntt_stream_t stream) {
+  t_launches = 0;
+  if (ntt_status st = check_transform_args(pl, x, batch); st != NTT_OK) return st;
+  if (inverse > 1 || pass >= pl->passes.size()) return NTT_ERR_ARG;
+  if (pl->bfly != NTT_BFLY_ALG3 && !inverse && pl->passes.size() > 1) return NTT_ERR_UNSUPPORTED;
+  if (!batch) return NTT_OK;
+  DeviceGuard g(pl->device);
+  if (!g.ok) return cuda_fail(cudaGetLastError());
+  cudaError_t e = run_pass(pl, x, batch, (cudaStream_t)stream, inverse != 0, pass);
+  ++t_launches;
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 
 ntt_status ntt_pointwise_mul(ntt_plan_t pl, void* c, const void* a, const void* b, size_t batch, unsigned flags,

@@ -1,6 +1,7 @@
 // tma.cuh -- Tensor Memory Accelerator / mbarrier PTX wrappers and the 128-byte
 // swizzle shared by the TMA-staged kernels (ntt_contig_tma.cu, ntt_cols_tma.cu).
 #pragma once
+#include "internal.h"
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -115,14 +116,13 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 inline int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
+  static PerDevice cache;
+  return cache.get([] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+    return n > 0 ? n : 148;
+  });
 }
 
 }  // namespace nttb

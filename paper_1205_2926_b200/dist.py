@@ -198,34 +198,85 @@ class FourStepInverseContig:
         return out
 
 
-class FourStepForwardP2P:
-    """FourStepForward with the all-to-all fused into the column pass over peer memory.
+class _P2PRecv:
+    """Receive buffers of a fused (peer-memory) exchange, double-buffered across calls.
 
-    The receive buffer is a symmetric-memory allocation (torch.distributed._symmetric_memory) rendezvoused
-    on `group`; `peer_ptrs` are every rank's receive-buffer addresses as seen from this device.  One call:
-    ntt_fourstep_cols_p2p (column NTTs + twiddle, rows stored into the peers' buffers), a stream-ordered
-    symmetric-memory barrier, ntt_fourstep_rows.  `recv`/`peer_ptrs` may be passed in directly (tests run
-    G virtual ranks on one GPU with ordinary buffers and no barrier)."""
+    Call k stores into buffer k mod 2 of every peer.  A rank can only reach the stores of call k+2
+    after the stream-ordered barrier of call k+1, which every peer enters after enqueueing its own
+    consumer of call k (rows / cols_inv) on the same stream, so a fast rank never overwrites a buffer
+    a slow peer is still reading (write-after-read across calls).  With a symmetric-memory handle the
+    two buffers are the halves of one rendezvoused allocation.  Virtual-rank tests pass `recv` (one
+    tensor, or a pair) and `peer_ptrs` (one list of addresses, or a pair of lists) directly."""
 
-    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None, recv=None, peer_ptrs=None, dtype=None):
-        self.plan, self.layout, self.rank, self.group = plan, layout, rank, group
+    def __init__(self, plan, layout, group, recv, peer_ptrs, dtype):
         self.hdl = None
         if recv is None:
             import torch
             import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm
             dt = dtype or (torch.uint64 if plan.word_bytes == 8 else torch.uint32)
-            self.recv = symm.empty(layout.shard_words, dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
-            self.hdl = symm.rendezvous(self.recv, group or dist.group.WORLD)
-            self.peer_ptrs = list(self.hdl.buffer_ptrs)
+            n = layout.shard_words
+            buf = symm.empty(2 * n, dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
+            self.hdl = symm.rendezvous(buf, group or dist.group.WORLD)
+            base = list(self.hdl.buffer_ptrs)
+            self.bufs = [buf[:n], buf[n:]]
+            self.ptr_sets = [base, [b + n * plan.word_bytes for b in base]]
+        elif isinstance(recv, (list, tuple)):
+            self.bufs = list(recv)
+            self.ptr_sets = [list(pp) for pp in peer_ptrs]
         else:
-            self.recv, self.peer_ptrs = recv, list(peer_ptrs)
+            self.bufs = [recv]
+            self.ptr_sets = [list(peer_ptrs)]
+        assert len(self.bufs) == len(self.ptr_sets)
+        self.calls = 0
+        self.cur = 0
+
+    def next(self):
+        """Buffer index of the next call (the producer side of the exchange)."""
+        self.cur = self.calls % len(self.bufs)
+        self.calls += 1
+        return self.cur
+
+    def barrier(self, stream):
+        """Cross-rank barrier, enqueued on `stream` (the kernels' stream), after this rank's stores."""
+        if self.hdl is None:
+            return
+        import torch
+        if stream is None:
+            self.hdl.barrier(channel=0)
+        else:
+            s = torch.cuda.ExternalStream(stream) if isinstance(stream, int) else stream
+            with torch.cuda.stream(s):
+                self.hdl.barrier(channel=0)
+
+
+class FourStepForwardP2P:
+    """FourStepForward with the all-to-all fused into the column pass over peer memory.
+
+    The receive buffers are a symmetric-memory allocation (torch.distributed._symmetric_memory) rendezvoused
+    on `group`, double-buffered across calls (_P2PRecv).  One call: ntt_fourstep_cols_p2p (column NTTs +
+    twiddle, rows stored into the peers' current buffer), a symmetric-memory barrier on the same stream,
+    ntt_fourstep_rows.  `recv`/`peer_ptrs` may be passed in directly (tests run G virtual ranks on one GPU
+    with ordinary buffers and no barrier)."""
+
+    def __init__(self, plan, layout: FourStepLayout, rank: int, group=None, recv=None, peer_ptrs=None, dtype=None):
+        self.plan, self.layout, self.rank, self.group = plan, layout, rank, group
+        self._rx = _P2PRecv(plan, layout, group, recv, peer_ptrs, dtype)
+        self.hdl = self._rx.hdl
+
+    @property
+    def recv(self):
+        return self._rx.bufs[self._rx.cur]
+
+    @property
+    def peer_ptrs(self):
+        return self._rx.ptr_sets[self._rx.cur]
 
     def cols_exchange(self, x_shard, stream=None):
-        self.plan.fourstep_cols_p2p(self.layout.ell1, x_shard, self.peer_ptrs, self.rank, self.layout.world,
+        i = self._rx.next()
+        self.plan.fourstep_cols_p2p(self.layout.ell1, x_shard, self._rx.ptr_sets[i], self.rank, self.layout.world,
                                     stream=stream)
-        if self.hdl is not None:
-            self.hdl.barrier(channel=0)  # every rank's stores into this buffer are visible
+        self._rx.barrier(stream)  # every rank's stores into this buffer are visible
 
     def rows(self, out, stream=None):
         self.plan.fourstep_rows(self.layout.ell1, self.recv, out, self.rank, self.layout.world, stream=stream)
@@ -238,35 +289,36 @@ class FourStepForwardP2P:
 
 class FourStepInverseP2P:
     """FourStepInverse with the all-to-all fused into the row pass (ntt_fourstep_rows_inv_p2p): each row's
-    natural-order inverse is scattered straight into the owning ranks' receive buffers over NVLink, a
-    stream-ordered symmetric-memory barrier, then ntt_fourstep_cols_inv on this rank's buffer, which ends
-    as the natural-order column shard of L*a.  `recv`/`peer_ptrs` may be passed in (virtual-rank tests)."""
+    natural-order inverse is scattered straight into the owning ranks' current receive buffer over NVLink
+    (double-buffered across calls, _P2PRecv), a symmetric-memory barrier on the same stream, then
+    ntt_fourstep_cols_inv on this rank's buffer, which ends as the natural-order column shard of L*a.
+    The returned buffer stays valid until the call after next.  `recv`/`peer_ptrs` may be passed in
+    (virtual-rank tests)."""
 
     def __init__(self, plan, layout: FourStepLayout, rank: int, group=None, recv=None, peer_ptrs=None, dtype=None):
         self.plan, self.layout, self.rank = plan, layout, rank
-        self.hdl = None
-        if recv is None:
-            import torch
-            import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm
-            dt = dtype or (torch.uint64 if plan.word_bytes == 8 else torch.uint32)
-            self.recv = symm.empty(layout.shard_words, dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
-            self.hdl = symm.rendezvous(self.recv, group or dist.group.WORLD)
-            self.peer_ptrs = list(self.hdl.buffer_ptrs)
-        else:
-            self.recv, self.peer_ptrs = recv, list(peer_ptrs)
+        self._rx = _P2PRecv(plan, layout, group, recv, peer_ptrs, dtype)
+        self.hdl = self._rx.hdl
+
+    @property
+    def recv(self):
+        return self._rx.bufs[self._rx.cur]
+
+    @property
+    def peer_ptrs(self):
+        return self._rx.ptr_sets[self._rx.cur]
 
     def rows_exchange(self, rows, stream=None):
-        self.plan.fourstep_rows_inv_p2p(self.layout.ell1, rows, self.peer_ptrs, self.rank, self.layout.world,
+        i = self._rx.next()
+        self.plan.fourstep_rows_inv_p2p(self.layout.ell1, rows, self._rx.ptr_sets[i], self.rank, self.layout.world,
                                         stream=stream)
-        if self.hdl is not None:
-            self.hdl.barrier(channel=0)
+        self._rx.barrier(stream)
 
     def cols_inv(self, stream=None):
         self.plan.fourstep_cols_inv(self.layout.ell1, self.recv, self.rank, self.layout.world, stream=stream)
 
     def __call__(self, rows, stream=None):
-        """Returns self.recv, which then holds the natural-order column shard of L*a."""
+        """Returns the current receive buffer, which then holds the natural-order column shard of L*a."""
         self.rows_exchange(rows, stream)
         self.cols_inv(stream)
         return self.recv

@@ -160,6 +160,8 @@ def test_block_transpose(ntt):
 
 @pytest.mark.parametrize("p,bits,ell,ell1,G", [
     (P62, 64, 12, 6, 2), (P62, 64, 16, 8, 4), (P30, 32, 16, 8, 2), (P62, 64, 20, 10, 8), (P62, 64, 28, 14, 8),
+    # one-round column passes (R == 1: u64 2^4, u32 2^4 / 2^5), whose prefetch is not behind a round barrier
+    (P62, 64, 10, 4, 2), (P30, 32, 10, 4, 2), (P30, 32, 12, 5, 2),
 ])
 def test_fourstep_p2p_virtual_ranks(ntt, p, bits, ell, ell1, G):
     """Fused column pass + all-to-all (ntt_fourstep_cols_p2p): G virtual ranks on one GPU whose 'peer'
@@ -248,3 +250,41 @@ def test_fourstep_inverse_p2p_virtual_ranks(ntt, p, bits, ell, ell1, G):
         ranks[g].cols_inv()
         want = ref.view(N1, N2)[:, g * Wl:(g + 1) * Wl].contiguous().view(-1)
         assert _ieq(recvs[g], want, bits), g
+
+
+@pytest.mark.parametrize("p,bits,ell,ell1,G", [(P62, 64, 16, 8, 2), (P30, 32, 16, 8, 4)])
+def test_fourstep_p2p_calls_overlap_across_ranks(ntt, p, bits, ell, ell1, G):
+    """Write-after-read across calls: rank 0's call k+1 (its stores into every peer's receive buffer) is
+    enqueued before rank 1..G-1 read call k's data.  The double-buffered receive side (_P2PRecv) keeps
+    both calls' results equal to ntt_forward; single-buffered, call k+1 would overwrite call k."""
+    from paper_1205_2926_b200.dist import FourStepForwardP2P, FourStepLayout
+    import synth
+    lay = FourStepLayout(ell, ell1, G)
+    L, N1, N2, Wl = lay.L, lay.N1, lay.N2, lay.local_width
+    w = pow(3, (p - 1) // L, p)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    xs, refs = [], []
+    for k in range(2):
+        x = torch.empty(L, dtype=dt, device="cuda")
+        ntt.synth_uniform(x, synth.config_seed(5), 10 + k, bound=p)
+        r = x.clone()
+        plan.forward(r)
+        xs.append([x.view(N1, N2)[:, g * Wl:(g + 1) * Wl].contiguous().view(-1) for g in range(G)])
+        refs.append(r)
+    recvs = [[torch.full((lay.shard_words,), 7, dtype=dt, device="cuda") for _ in range(2)] for _ in range(G)]
+    ptrs = [[recvs[g][i].data_ptr() for g in range(G)] for i in range(2)]
+    ranks = [FourStepForwardP2P(plan, lay, g, recv=recvs[g], peer_ptrs=ptrs) for g in range(G)]
+    outs = [[torch.empty(lay.shard_words, dtype=dt, device="cuda") for _ in range(G)] for _ in range(2)]
+    for g in range(G):
+        ranks[g].cols_exchange(xs[0][g])           # call 0, every rank
+    ranks[0].rows(outs[0][0])
+    ranks[0].cols_exchange(xs[1][0])               # rank 0 races ahead into call 1 ...
+    for g in range(1, G):
+        ranks[g].rows(outs[0][g])                  # ... before its peers read call 0
+    for g in range(1, G):
+        ranks[g].cols_exchange(xs[1][g])
+    for g in range(G):
+        ranks[g].rows(outs[1][g])
+    for k in range(2):
+        assert _ieq(torch.cat(outs[k]), refs[k], bits), k

@@ -550,3 +550,33 @@ def test_cyclic_convolution_other_shapes(ntt, bits, p, ell, batch):
         assert np.array_equal(got[i], ref)
         for k in (0, 1, L // 2, L - 1):
             assert int(got[i, k]) == oracle.cyclic_conv_coeff(p, a[i], b[i], k)
+
+
+# ---------------------------------------------------------------- pass-by-pass entry point
+@pytest.mark.parametrize("p,bits,ell,batch", [(P62, 64, 12, 5), (P62, 64, 20, 2), (P30, 32, 22, 1),
+                                              (P62, 64, 25, 1)])
+def test_transform_pass_sequence_equals_transform(ntt, p, bits, ell, batch):
+    """ntt_transform_pass over the schedule (forward 0..n-1, inverse n-1..0) = ntt_forward / ntt_inverse,
+    and the forward equals the oracle (bench.py times multi-pass configs pass by pass)."""
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    n = plan.info().n_passes
+    x = rand_residues(np.random.default_rng(ell), p, (batch, L))
+    a, b = to_dev(x, bits), to_dev(x, bits)
+    plan.forward(a)
+    for j in range(n):
+        plan.transform_pass(b, j)
+    fa = to_host(a)
+    assert np.array_equal(fa, to_host(b))
+    if L <= 1 << 20:
+        assert np.array_equal(fa, oracle.ntt_forward(p, w, x, nthreads=NTHREADS))
+    else:
+        for j in (0, 1, L - 1, 12345):
+            assert int(fa[0, j]) == oracle.ntt_output_at(p, w, x[0], j)
+    plan.inverse(a)
+    for j in reversed(range(n)):
+        plan.transform_pass(b, j, inverse=True)
+    assert np.array_equal(to_host(a), to_host(b))
+    with pytest.raises(ntt.NttError):
+        plan.transform_pass(b, n)
