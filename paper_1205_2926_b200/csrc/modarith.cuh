@@ -128,6 +128,19 @@ template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W 
   bfly_alg4<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u, 0});
 }
 
+// Algorithm 4 given the NEGATED twiddle (wn, wn') = (-W mod p, its Shoup W'), as read from the
+// forward table (omega^{-e} = -omega^{N/2-e}, so no inverse table is stored):
+// T~ = Shoup(wn, Y) = -WY mod p in [0,2p), and the two outputs of lines 4-5 swap their formulas:
+// X' = X - T~ + 2p = X + WY, Y' = X + T~ = X - WY (mod p), both still in [0,4p) (Theorem 3's
+// bounds, with T~ in place of T).
+template <class W, bool PLO1 = false>
+__device__ __forceinline__ void bfly_alg4n(W& X, W& Y, W wn, W wnp, const Mod<W>& m) {
+  W x = csub<W>(X, m.p2);                       // line 1
+  W T = shoup_mul<W, PLO1, true>(Y, wn, wnp, m);  // lines 2-3 with -W
+  X = x - T + m.p2;
+  Y = x + T;
+}
+
 // W = 1 inverse butterfly: T = Y reduced once by 2p (Y < 4p -> T < 2p).
 template <class W> __device__ __forceinline__ void bfly_alg4_w1(W& X, W& Y, W p2) {
   W x = csub<W>(X, p2);

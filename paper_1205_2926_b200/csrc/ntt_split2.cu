@@ -228,7 +228,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
   constexpr int S = 1 << SR, G = Sh::E >> SR;
   constexpr int D = Q >> (LEVEL + SR), B = Q >> LEVEL;
-  const TwPair<W>* tw_sub = tw_full + ((1 << LOGL) - Q);  // stages s+1..ell of the full per-stage table
+  const TwPair<W>* tw_sub = tw_full + stage_off(LOGL, SS + 1);  // stages s+1..ell of the full per-stage table
   constexpr bool REMAP = !INV && split_remap_last<LOGQ, LE, r>();  // this round: remapped groups
   int c[G], blk[G];
 #pragma unroll
@@ -434,6 +434,10 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         constexpr int U = sizeof(W) == 4 ? 8 : 4;
         static_assert(H2 % U == 0, "whole groups");
         auto finish = [&](const W* mine_v, bool r0) {
+          // -zeta_1^{-j} at entry Q - j of stage 1 (inv_index); the per-thread base is made opaque here
+          // so its address arithmetic is not hoisted above the rounds (register pressure)
+          uint32_t jr = (uint32_t)(off + Q - (r0 ? 0 : PER_CTA) - t);
+          asm volatile("" : "+r"(jr));
 #pragma unroll
           for (int h0 = 0; h0 < H2; h0 += U) {
             W u0[U], u1[U], w[U], wp[U];
@@ -443,12 +447,12 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
               const W theirs = sm[(h0 + u) * D + t];
               u0[u] = r0 ? mine_v[h0 + u] : theirs;  // x_j sits in CTA 0, x_{j+Q} in CTA 1
               u1[u] = r0 ? theirs : mine_v[h0 + u];
-              ldtw<W>(tw_full, (uint32_t)(off + j), w[u], wp[u]);
+              ldtw<W>(tw_full, jr - (uint32_t)((h0 + u) * D), w[u], wp[u]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const int j = (r0 ? 0 : PER_CTA) + (h0 + u) * D + t;
-              bfly_alg4<W, PLO1>(u0[u], u1[u], w[u], wp[u], m);
+              bfly_alg4n<W, PLO1>(u0[u], u1[u], w[u], wp[u], m);
               xb[j] = norm4<W>(u0[u], m.p, m.p2);
               xb[j + Q] = norm4<W>(u1[u], m.p, m.p2);
             }
@@ -484,8 +488,8 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
               for (int tt = 0; tt < half; ++tt) {
                 W w, wp;
-                ldtw<W>(tw_full, (uint32_t)(off + j + tt * Q), w, wp);
-                bfly_alg4<W, PLO1>(u[bb + tt], u[bb + tt + half], w, wp, m);
+                ldtw<W>(tw_full, (uint32_t)(off + ((1 << LOGL) >> i) - (j + tt * Q)), w, wp);  // inv_index
+                bfly_alg4n<W, PLO1>(u[bb + tt], u[bb + tt + half], w, wp, m);
               }
           }
 #pragma unroll

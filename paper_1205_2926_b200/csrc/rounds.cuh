@@ -31,8 +31,18 @@ template <> __device__ __forceinline__ void ldtw<uint32_t>(const TwPair<uint32_t
   wp = t.y;
 }
 
-// Offset of stage i's table inside the per-stage layout of an N-point transform.
-__host__ __device__ constexpr int stage_off(int logn, int i) { return (1 << logn) - ((1 << logn) >> (i - 1)); }
+// Offset of stage i's table inside the per-stage layout of an N-point transform: stage i holds
+// zeta_i^k for k <= m_i = N >> i (m_i + 1 entries; the last one is zeta_i^{m_i} = omega^{N/2} = -1).
+__host__ __device__ constexpr int stage_off(int logn, int i) {
+  return (1 << logn) - ((1 << logn) >> (i - 1)) + (i - 1);
+}
+
+// The inverse reads the same table (no second table).  zeta_i^{-k} = -zeta_i^{m_i - k}
+// (zeta_i^{m_i} = omega^{N/2} = -1), so entry m_i - k holds (W~, W~') with W~ = -zeta_i^{-k} mod p,
+// and the inverse butterfly bfly_alg4n takes the negated twiddle.  Index of that entry:
+__host__ __device__ constexpr int inv_index(int logn, int i, int k) {
+  return stage_off(logn, i) + ((1 << logn) >> i) - k;
+}
 
 // Round structure: R rounds of balanced stage counts sr(r) <= LE.
 template <int LOGN, int LE> struct Rounds {
@@ -101,8 +111,8 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
   }
 }
 
-// Inverse round: the same stages run backwards, Algorithm 4 with the
-// inverse table zeta_i^{-k}.
+// Inverse round: the same stages run backwards, Algorithm 4 with the twiddles
+// zeta_i^{-k}, read as their negations from the forward table (inv_index, bfly_alg4n).
 template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
 __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, const Mod<W>& m) {
   constexpr int S = 1 << SR;
@@ -118,12 +128,13 @@ __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* _
       for (int hh = 0; hh < half; ++hh) {
         const bool unit = w1 || (D == 1 && hh == 0);  // k = 0: W = 1
         W w = 1, wp = 0;
-        if (!unit) ldtw<W>(twi, (uint32_t)(off + hh * D + c[q]), w, wp);
+        // negated twiddle -zeta^{-k} = zeta^{m - k} from the forward table (inv_index)
+        if (!unit) ldtw<W>(twi, (uint32_t)(off + ((1 << LOGN) >> (LEVEL + j + 1)) - (hh * D + c[q])), w, wp);
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
           if (unit) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
-          else bfly_alg4<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          else bfly_alg4n<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
         }
       }
     }
