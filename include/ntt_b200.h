@@ -257,6 +257,24 @@ ntt_status ntt_calibrate_butterfly(unsigned log2_beta, uint64_t p, uint64_t W, u
  * read of the data and a host round trip per call.  Returns the previous setting. */
 unsigned ntt_set_range_checks(unsigned on);
 
+/* Range audit (a debugging build, libntt_b200_audit.so, compiled with
+ * -DNTT_RANGE_AUDIT).  In that build every butterfly checks the intervals of its theorem --
+ * Theorem 2: Algorithm 3 inputs/outputs in [0,2p) and T = X - Y + 2p in [0,4p);
+ * Theorem 3: Algorithm 4 in [0,4p); Theorem 4: Algorithm 5 outputs in
+ * [0,2p); Algorithm 2 canonical -- every column pass checks the buffer it leaves in HBM (< 2p
+ * forward, < 4p inverse) and every normalised output is checked < p; each violation increments a
+ * device counter.
+ *   ntt_build_flags: NTT_BUILD_RANGE_AUDIT when this library is the audit build.
+ *   ntt_audit_counts: synchronises `device` and returns the violations counted since the last
+ *     reset.  NTT_ERR_UNSUPPORTED in the production build.
+ *   ntt_audit_reset: synchronises, zeroes the counters; mutate != 0 drops the "+2p" of Algorithm 3
+ *     line 3 in every kernel (the mutation control), which the audit must report.
+ *     NTT_ERR_UNSUPPORTED in the production build. */
+#define NTT_BUILD_RANGE_AUDIT 1u
+unsigned ntt_build_flags(void);
+ntt_status ntt_audit_counts(int device, uint64_t* violations);
+ntt_status ntt_audit_reset(int device, int mutate);
+
 /* Number of kernel launches the last transform entry point on this thread issued. */
 unsigned ntt_last_launch_count(void);
 const char* ntt_status_str(ntt_status s);

@@ -11,7 +11,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("NTT_B200_LIB") or os.path.join(_HERE, "libntt_b200.so")
+# NTT_B200_LIB: a library path, or "audit" for the range-audit debug build (libntt_b200_audit.so)
+_LIB_ENV = os.environ.get("NTT_B200_LIB", "")
+LIB_PATH = (os.path.join(_HERE, "libntt_b200_audit.so") if _LIB_ENV == "audit"
+            else (_LIB_ENV or os.path.join(_HERE, "libntt_b200.so")))
 
 NTT_SCALE_INV_L = 1
 NTT_OP_FORWARD = 1
@@ -71,6 +74,8 @@ def _load() -> ctypes.CDLL:
         "ntt_debug_butterfly": [vp, c_int, vp, vp, vp, vp, sz, vp],
         "ntt_execute_host": [vp, uint, vp, vp, sz, vp, sz, vp],
         "ntt_calibrate_butterfly": [uint, u64, u64, u64, uint, vp, ctypes.POINTER(u64), vp],
+        "ntt_audit_counts": [c_int, ctypes.POINTER(u64)],
+        "ntt_audit_reset": [c_int, c_int],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -83,6 +88,7 @@ def _load() -> ctypes.CDLL:
     lib.ntt_set_range_checks.argtypes = [uint]
     lib.ntt_set_range_checks.restype = uint
     lib.ntt_abi_version.restype = uint
+    lib.ntt_build_flags.restype = uint
     return lib
 
 
@@ -93,7 +99,7 @@ EXPORTED = (
     "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
     "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p",
     "ntt_fourstep_rows_inv_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
-    "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_set_range_checks", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
+    "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_set_range_checks", "ntt_build_flags", "ntt_audit_counts", "ntt_audit_reset", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
 )
 
 
@@ -139,6 +145,23 @@ def _stream(stream) -> int:
 def set_range_checks(on: bool) -> bool:
     """ntt_set_range_checks: debugging mode validating transform inputs (returns the previous setting)."""
     return bool(_lib.ntt_set_range_checks(1 if on else 0))
+
+
+def audit_build() -> bool:
+    """True when the loaded library is the range-audit debug build (NTT_B200_LIB=audit)."""
+    return bool(_lib.ntt_build_flags() & 1)
+
+
+def audit_counts(device: int = 0) -> int:
+    """ntt_audit_counts: range violations counted since the last audit_reset (audit build only)."""
+    v = ctypes.c_uint64()
+    _check(_lib.ntt_audit_counts(device, ctypes.byref(v)), "ntt_audit_counts")
+    return int(v.value)
+
+
+def audit_reset(device: int = 0, mutate: bool = False):
+    """ntt_audit_reset: zero the counters; mutate drops Algorithm 3's "+2p" (audit build only)."""
+    _check(_lib.ntt_audit_reset(device, 1 if mutate else 0), "ntt_audit_reset")
 
 
 def last_launch_count() -> int:

@@ -43,6 +43,40 @@ __device__ __forceinline__ W fourstep_twiddle_ct(W val, uint32_t e, uint32_t H, 
   }
 }
 
+// The same for the ablation butterflies (BF 2: Shoup pairs, canonical result; BF 5: one-word
+// Montgomery tables, Algorithm 5's multiply), factored (FACT) or direct tables.
+template <class W, bool PLO1, bool FACT, int BF>
+__device__ __forceinline__ W fourstep_twiddle_bf(W val, uint32_t e, uint32_t H, const TwPair<W>* __restrict__ fa,
+                                                 const TwPair<W>* __restrict__ fb, const Mod<W>& m) {
+  if constexpr (BF == 3) {
+    return fourstep_twiddle_ct<W, PLO1, FACT>(val, e, H, fa, fb, m);
+  } else if constexpr (!FACT) {
+    W w, wp;
+    ldtw_bf<W, BF>(fa, e, w, wp);
+    return twiddle_mul<W, PLO1, BF>(val, w, wp, m);
+  } else {
+    W w, wp, w2, wp2;
+    ldtw_bf<W, BF>(fb, e & ((1u << H) - 1), w, wp);
+    ldtw_bf<W, BF>(fa, e >> H, w2, wp2);
+    val = twiddle_mul<W, PLO1, BF>(val, w, wp, m);
+    return twiddle_mul<W, PLO1, BF>(val, w2, wp2, m);
+  }
+}
+
+// Block index and column group of a column-pass tile (ColsParams::bmajor: DESIGN.md §5).
+// BM: the kernel supports the block-major order (only the twiddle-matrix instantiations do).
+template <bool BM = true>
+__device__ __forceinline__ void cols_tile_coords(uint64_t tile, const ColsParams& prm, uint64_t& bq, uint32_t& cg) {
+  if (!BM || !prm.bmajor) {
+    bq = tile >> prm.log_colgroups;
+    cg = (uint32_t)(tile & ((1ull << prm.log_colgroups) - 1));
+  } else {
+    const uint64_t nblk = prm.n_tiles >> prm.log_colgroups, rest = tile >> prm.log_cgi;
+    bq = rest % nblk;
+    cg = ((uint32_t)(rest / nblk) << prm.log_cgi) | (uint32_t)(tile & ((1u << prm.log_cgi) - 1));
+  }
+}
+
 // Global column of local column `cloc` (ColsParams.shard: config C5 column shard).
 __device__ __forceinline__ uint32_t cols_global_column(uint32_t cloc, const ColsParams& prm) {
   if (!prm.shard) return cloc;

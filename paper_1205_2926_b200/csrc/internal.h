@@ -27,6 +27,15 @@ struct PerDevice {
   }
 };
 
+// Range-audit build (-DNTT_RANGE_AUDIT, modarith.cuh): each kernel translation unit registers the
+// host accessors of its device counter; plan.cu sums them (ntt_audit_counts).
+struct AuditTU {
+  unsigned long long (*read)();
+  void (*reset)();
+  void (*mutate)(int);
+};
+void audit_register(const AuditTU& tu);
+
 // Limits of the on-chip (single-pass) transform and of the column pass, as
 // log2 of the sub-transform length, per word size.
 constexpr int kContigMaxLog64 = 14;  // 2^14 u64 = 128 KiB smem, 512 threads x 32 words
@@ -67,6 +76,16 @@ struct ColsParams {
   uint32_t log_rows_rank;  // log2(N1/G)
   uint32_t src_rank;
   uint64_t peer[8];        // receive buffers of the G <= 8 ranks (device addresses)
+  // forward four-step twiddle from the pass's twiddle matrix DevTables::fm (N x S, row-major,
+  // M[r][c] = omega_B^{c rev(r)}): one load and one Shoup product per element (k_cols_tma only;
+  // other kernels use the factored tables fa/fb, which the plan always keeps)
+  uint32_t matrix;
+  // tile order: 0 = column groups fastest (tile = block * groups + group); 1 = blocks fastest within
+  // runs of 2^log_cgi column groups, so the CTAs in flight share a few column groups' twiddle rows
+  uint32_t bmajor;
+  uint32_t log_cgi;
+  // forward butterfly of the plan (3 = Algorithm 3; 2 / 5 = the ablations F1 / F2, forward only)
+  uint32_t bf;
 };
 
 struct DevTables {
@@ -74,6 +93,7 @@ struct DevTables {
   const void* sub_inv;  // omega_N^{-e}
   const void* fa;       // factored four-step table A (or the direct table when H == 0)
   const void* fb;       // factored four-step table B
+  const void* fm = nullptr;  // forward four-step twiddle matrix (ColsParams::matrix)
 };
 
 // launchers (return cudaGetLastError of the launch)
@@ -88,7 +108,7 @@ cudaError_t launch_contig_tma(int wbytes, int logn, bool inverse, bool normalize
 bool split2_supported(int wbytes, int logn);
 cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
                           const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s,
-                          const void* tw1s = nullptr);
+                          const void* tw1s = nullptr, int bf = 3);
 cudaError_t launch_cols(int wbytes, int logn, bool inverse, void* x, const ColsParams& prm, const DevTables& t,
                         uint64_t p, cudaStream_t s);
 // the same pass with TMA-staged, double-buffered tiles (ntt_cols_tma.cu)

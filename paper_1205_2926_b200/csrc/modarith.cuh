@@ -6,7 +6,53 @@
 #pragma once
 #include <cstdint>
 
+#ifdef NTT_RANGE_AUDIT
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#endif
+
 namespace nttb {
+
+// ---- range audit (debug build, -DNTT_RANGE_AUDIT) ----
+// Every butterfly checks the intervals its theorem states -- Theorem 2: Alg. 3 inputs
+// and outputs in [0,2p), T = X - Y + 2p in [0,4p); Theorem 3: Alg. 4 in [0,4p);
+// Theorem 4: Alg. 5 outputs in [0,2p); Alg. 2 canonical -- and the column passes check
+// the buffers they leave in HBM (< 2p forward, < 4p inverse) and every normalised output (< p).  A
+// violation increments a per-translation-unit device counter, read through ntt_audit_counts().
+// d_audit_mutate = 1 drops the "+2p" of Alg. 3 line 3 (SPEC's mutation control), which the T check
+// must report.  The production build compiles all of this away.
+#ifdef NTT_RANGE_AUDIT
+namespace {
+__device__ unsigned long long d_audit_count;
+__device__ unsigned long long d_audit_checks;
+__device__ int d_audit_mutate;
+unsigned long long audit_read_tu() {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, d_audit_count, sizeof v);
+  return v;
+}
+void audit_reset_tu() {
+  const unsigned long long z = 0;
+  cudaMemcpyToSymbol(d_audit_count, &z, sizeof z);
+}
+void audit_mutate_tu(int on) { cudaMemcpyToSymbol(d_audit_mutate, &on, sizeof on); }
+struct AuditReg {
+  AuditReg() { audit_register(AuditTU{audit_read_tu, audit_reset_tu, audit_mutate_tu}); }
+} audit_reg_instance;
+}  // namespace
+// one predicated reduction, no C++ control flow (keeps the instrumented kernels quick to compile)
+__device__ __forceinline__ void audit_lt(uint64_t x, uint64_t bound) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.u64 p, %0, %1;\n\t@p red.global.add.u64 [%2], 1;\n\t}"
+               :: "l"(x), "l"(bound), "l"(&d_audit_count) : "memory");
+}
+__device__ __forceinline__ bool audit_mutated() { return *(volatile int*)&d_audit_mutate != 0; }
+#define NTT_AUDIT(x, b) ::nttb::audit_lt((uint64_t)(x), (uint64_t)(b))
+#define NTT_AUDIT_MUTATED() ::nttb::audit_mutated()
+#else
+#define NTT_AUDIT(x, b) ((void)0)
+#define NTT_AUDIT_MUTATED() false
+#endif
 
 template <class W> struct TwPair;               // (W, W') twiddle pair, stored adjacently
 template <> struct alignas(8) TwPair<uint32_t> { uint32_t w, wp; };
@@ -97,10 +143,16 @@ template <class W> __device__ __forceinline__ W shoup_mul(W T, W w, W wp, W p) {
 // X, Y in [0,2p) -> X' = X+Y, Y' = W(X-Y), both in [0,2p)  (Theorem 2).
 template <class W, bool PLO1 = false>
 __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  NTT_AUDIT(X, m.p2);
+  NTT_AUDIT(Y, m.p2);
   W s = csub<W>(X + Y, m.p2);  // lines 1-2
   W T = X - Y + m.p2;          // line 3: T in [0,4p), no correction
+  if (NTT_AUDIT_MUTATED()) T = X - Y;  // mutation control (audit build only)
+  NTT_AUDIT(T, 2 * m.p2);
   Y = shoup_mul<W, PLO1>(T, w, wp, m);  // lines 4-5: [0,2p), no correction
   X = s;
+  NTT_AUDIT(X, m.p2);
+  NTT_AUDIT(Y, m.p2);
 }
 template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W wp, W p, W p2) {
   bfly_alg3<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u, 0});
@@ -109,20 +161,32 @@ template <class W> __device__ __forceinline__ void bfly_alg3(W& X, W& Y, W w, W 
 // W = 1 butterflies (O(L) butterflies have W = 1 and are cheaper):
 // X' as in Alg. 3, Y' = T reduced once by 2p, so Y' in [0,2p), no multiply.
 template <class W> __device__ __forceinline__ void bfly_alg3_w1(W& X, W& Y, W p2) {
+  NTT_AUDIT(X, p2);
+  NTT_AUDIT(Y, p2);
   W s = csub<W>(X + Y, p2);
-  W T = csub<W>(X - Y + p2, p2);
+  W T0 = X - Y + p2;
+  if (NTT_AUDIT_MUTATED()) T0 = X - Y;
+  NTT_AUDIT(T0, 2 * p2);
+  W T = csub<W>(T0, p2);
   X = s;
   Y = T;
+  NTT_AUDIT(X, p2);
+  NTT_AUDIT(Y, p2);
 }
 
 // Algorithm 4, the modified inverse butterfly:
 // X, Y in [0,4p) -> X' = X + WY, Y' = X - WY, both in [0,4p)  (Theorem 3).
 template <class W, bool PLO1 = false>
 __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  NTT_AUDIT(X, 2 * m.p2);
+  NTT_AUDIT(Y, 2 * m.p2);
   W x = csub<W>(X, m.p2);                   // line 1
   W T = shoup_mul<W, PLO1, true>(Y, w, wp, m);  // lines 2-3: Y < 4p < beta is a legal Shoup input
+  NTT_AUDIT(T, m.p2);
   X = x + T;
   Y = x - T + m.p2;
+  NTT_AUDIT(X, 2 * m.p2);
+  NTT_AUDIT(Y, 2 * m.p2);
 }
 template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W wp, W p, W p2) {
   bfly_alg4<W, false>(X, Y, w, wp, Mod<W>{p, p2, 0u, 0});
@@ -135,18 +199,27 @@ template <class W> __device__ __forceinline__ void bfly_alg4(W& X, W& Y, W w, W 
 // bounds, with T~ in place of T).
 template <class W, bool PLO1 = false>
 __device__ __forceinline__ void bfly_alg4n(W& X, W& Y, W wn, W wnp, const Mod<W>& m) {
+  NTT_AUDIT(X, 2 * m.p2);
+  NTT_AUDIT(Y, 2 * m.p2);
   W x = csub<W>(X, m.p2);                       // line 1
   W T = shoup_mul<W, PLO1, true>(Y, wn, wnp, m);  // lines 2-3 with -W
+  NTT_AUDIT(T, m.p2);
   X = x - T + m.p2;
   Y = x + T;
+  NTT_AUDIT(X, 2 * m.p2);
+  NTT_AUDIT(Y, 2 * m.p2);
 }
 
 // W = 1 inverse butterfly: T = Y reduced once by 2p (Y < 4p -> T < 2p).
 template <class W> __device__ __forceinline__ void bfly_alg4_w1(W& X, W& Y, W p2) {
+  NTT_AUDIT(X, 2 * p2);
+  NTT_AUDIT(Y, 2 * p2);
   W x = csub<W>(X, p2);
   W T = csub<W>(Y, p2);
   X = x + T;
   Y = x - T + p2;
+  NTT_AUDIT(X, 2 * p2);
+  NTT_AUDIT(Y, 2 * p2);
 }
 
 // Algorithm 2, NTL's butterfly, canonical [0,p) in and out (ablation F1).
@@ -162,12 +235,18 @@ template <class W> __device__ __forceinline__ void bfly_alg2(W& X, W& Y, W w, W 
 // Algorithm 2 inside the transform kernels (ablation F1), same Shoup core as Alg. 3.
 template <class W, bool PLO1>
 __device__ __forceinline__ void bfly_alg2m(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  NTT_AUDIT(X, m.p);
+  NTT_AUDIT(Y, m.p);
   W s = csub<W>(X + Y, m.p);                        // lines 1-2
   W T = (X < Y) ? X - Y + m.p : X - Y;               // lines 3-4 (X < Y realises T < 0)
   Y = csub<W>(shoup_mul<W, PLO1>(T, w, wp, m), m.p);  // lines 5-7
   X = s;
+  NTT_AUDIT(X, m.p);
+  NTT_AUDIT(Y, m.p);
 }
 template <class W> __device__ __forceinline__ void bfly_alg2_w1(W& X, W& Y, W p) {
+  NTT_AUDIT(X, p);
+  NTT_AUDIT(Y, p);
   W s = csub<W>(X + Y, p);
   Y = (X < Y) ? X - Y + p : X - Y;
   X = s;
@@ -198,12 +277,62 @@ template <class W> __device__ __forceinline__ void bfly_alg5(W& X, W& Y, W wm, W
 }
 
 template <class W> __device__ __forceinline__ void bfly_alg5m(W& X, W& Y, W wm, const Mod<W>& m) {
+  NTT_AUDIT(X, m.p2);
+  NTT_AUDIT(Y, m.p2);
   bfly_alg5<W>(X, Y, wm, m.J, m.p, m.p2);
+  NTT_AUDIT(X, m.p2);
+  NTT_AUDIT(Y, m.p2);
+}
+
+// Algorithm 5's multiply alone (lines 4-7): T * W mod p for wm = beta W mod p, any T < beta
+// (R1 < p because wm < p), result in (0, 2p).  The four-step twiddle product of Alg. 5 plans.
+template <class W> __device__ __forceinline__ W mont_mul(W T, W wm, const Mod<W>& m) {
+  W R1, R0;
+  mul_wide(wm, T, R1, R0);
+  W Q = R0 * m.J;
+  W H = mulhi(Q, m.p);
+  return R1 - H + m.p;
+}
+
+// The forward butterfly of a plan (BF: 3 = Algorithm 3, the hot path; 2 = Algorithm 2 and 5 =
+// Algorithm 5, the ablations F1 / F2 of SURVEY.md 8(f)).  (w, wp): the (W, W') pair; Alg. 5 uses w
+// only, holding beta W mod p.
+template <class W, bool PLO1, int BF>
+__device__ __forceinline__ void bfly_fwd(W& X, W& Y, W w, W wp, const Mod<W>& m) {
+  if constexpr (BF == 2) bfly_alg2m<W, PLO1>(X, Y, w, wp, m);
+  else if constexpr (BF == 5) bfly_alg5m<W>(X, Y, w, m);
+  else bfly_alg3<W, PLO1>(X, Y, w, wp, m);
+}
+// ... its W = 1 case
+template <class W, int BF> __device__ __forceinline__ void bfly_fwd_w1(W& X, W& Y, const Mod<W>& m) {
+  if constexpr (BF == 2) bfly_alg2_w1<W>(X, Y, m.p);
+  else bfly_alg3_w1<W>(X, Y, m.p2);
+}
+// ... and its twiddle product T * W (four-step twiddle): Shoup (BF 2 keeps Algorithm 2's canonical
+// operands), Montgomery for BF 5.
+template <class W, bool PLO1, int BF>
+__device__ __forceinline__ W twiddle_mul(W T, W w, W wp, const Mod<W>& m) {
+  W r;
+  if constexpr (BF == 5) r = mont_mul<W>(T, w, m);
+  else if constexpr (BF == 2) r = csub<W>(shoup_mul<W, PLO1>(T, w, wp, m), m.p);
+  else r = shoup_mul<W, PLO1>(T, w, wp, m);
+  NTT_AUDIT(r, BF == 2 ? m.p : m.p2);
+  return r;
 }
 
 // Final normalisation: [0,2p) -> [0,p) and [0,4p) -> [0,p).
-template <class W> __device__ __forceinline__ W norm2(W x, W p) { return csub<W>(x, p); }
-template <class W> __device__ __forceinline__ W norm4(W x, W p, W p2) { return csub<W>(csub<W>(x, p2), p); }
+template <class W> __device__ __forceinline__ W norm2(W x, W p) {
+  NTT_AUDIT(x, 2 * p);
+  const W y = csub<W>(x, p);
+  NTT_AUDIT(y, p);
+  return y;
+}
+template <class W> __device__ __forceinline__ W norm4(W x, W p, W p2) {
+  NTT_AUDIT(x, 2 * p2);
+  const W y = csub<W>(csub<W>(x, p2), p);
+  NTT_AUDIT(y, p);
+  return y;
+}
 
 // Pointwise product of two data values (no reusable W', so no Shoup; P:21 use):
 // returns a*b*R^{-1}-style Montgomery REDC in the Alg. 5 pattern:

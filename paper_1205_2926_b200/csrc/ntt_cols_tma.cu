@@ -36,22 +36,25 @@ template <class W, int LOGN, int LE> struct ColsTmaShape {
   static_assert(TILE_BYTES % 1024 == 0, "tiles must keep the 1024-byte swizzle period");
 };
 
-template <class W, int LOGN, int LE>
-__device__ __forceinline__ void cols_tma_issue(const CUtensorMap* map, uint64_t tile, uint32_t log_colgroups,
+template <class W, int LOGN, int LE, bool BM>
+__device__ __forceinline__ void cols_tma_issue(const CUtensorMap* map, uint64_t tile, const ColsParams& prm,
                                                uint32_t buf, uint32_t bar) {
   using Sh = ColsTmaShape<W, LOGN, LE>;
-  const int bq = (int)(tile >> log_colgroups);
-  const int c0 = (int)(tile & ((1ull << log_colgroups) - 1)) * Sh::C;
+  uint64_t b64;
+  uint32_t cg;
+  cols_tile_coords<BM>(tile, prm, b64, cg);
+  const int bq = (int)b64, c0 = (int)cg * Sh::C;
   mbar_expect_tx(bar, Sh::TILE_BYTES);
 #pragma unroll
   for (int bx = 0; bx < Sh::BOXES; ++bx) tma_load_3d(buf + bx * Sh::BOX_ROWS * 128, map, c0, bx * Sh::BOX_ROWS, bq, bar);
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1, bool FACT, int r>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, int TWM, int BF, int r>
 __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint32_t cglob, const ColsParams& prm,
                                                const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
-                                               const TwPair<W>* __restrict__ fb, const Mod<W>& m,
-                                               const CUtensorMap* map, uint64_t next_tile, uint32_t next_buf,
+                                               const TwPair<W>* __restrict__ fb, const TwPair<W>* __restrict__ fm,
+                                               const Mod<W>& m, const CUtensorMap* map, uint64_t next_tile,
+                                               uint32_t next_buf,
                                                uint32_t next_bar, bool prefetch) {
   using Sh = ColsTmaShape<W, LOGN, LE>;
   using RC = typename Sh::RC;
@@ -85,17 +88,17 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
           const int row = blk[q] * B + h * D + c[q];
           const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
           const uint32_t e = (cglob * rv) << prm.log_tw_mul;
-          v[q * S + h] = fourstep_twiddle_ct<W, PLO1, FACT>(v[q * S + h], (0u - e) & emask, prm.H, fa, fb, m);
+          v[q * S + h] = fourstep_twiddle_ct<W, PLO1, TWM != 0>(v[q * S + h], (0u - e) & emask, prm.H, fa, fb, m);
         }
     }
   }
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF>(v, c, tw, m);
   else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (!last) {
     __syncthreads();
     if (prefetch && threadIdx.x == 0) {  // the other buffer's store has been issued: reuse it once read
       bulk_wait_read0();
-      cols_tma_issue<W, LOGN, LE>(map, next_tile, prm.log_colgroups, next_buf, next_bar);
+      cols_tma_issue<W, LOGN, LE, TWM == 2>(map, next_tile, prm, next_buf, next_bar);
     }
   }
   if constexpr (last) {
@@ -106,9 +109,15 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
           for (int h = 0; h < S; ++h) {
             const int row = blk[q] * B + h * D + c[q];
-            const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
-            v[q * S + h] = fourstep_twiddle_ct<W, PLO1, FACT>(v[q * S + h], (cglob * rv) << prm.log_tw_mul, prm.H, fa,
-                                                              fb, m);
+            if constexpr (TWM == 2) {  // twiddle matrix: M[row][c] = omega_B^{c rev(row)}, one product
+              W w, wp;
+              ldtw_bf<W, BF>(fm, ((uint32_t)row << prm.log_S) + cglob, w, wp);
+              v[q * S + h] = twiddle_mul<W, PLO1, BF>(v[q * S + h], w, wp, m);
+            } else {
+              const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
+              v[q * S + h] = fourstep_twiddle_bf<W, PLO1, TWM == 1, BF>(v[q * S + h], (cglob * rv) << prm.log_tw_mul,
+                                                                         prm.H, fa, fb, m);
+            }
           }
       }
       if (prm.normalize) {
@@ -122,6 +131,12 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
       }
     }
   }
+#ifdef NTT_RANGE_AUDIT
+  if constexpr (last) {  // the buffer this pass leaves for the next one (or the final output)
+#pragma unroll
+    for (int i = 0; i < Sh::E; ++i) NTT_AUDIT(v[i], prm.normalize ? m.p : (INV ? 2 * m.p2 : m.p2));
+  }
+#endif
 #pragma unroll
   for (int q = 0; q < G; ++q)
 #pragma unroll
@@ -132,15 +147,16 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
   if constexpr (!last) {
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, FACT, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, map, next_tile,
-                                                     next_buf, next_bar, false);
+    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, fm, m, map, next_tile,
+                                                    next_buf, next_bar, false);
   }
 }
 
-template <class W, int LOGN, int LE, bool INV, bool PLO1, bool P2P, bool FACT>
+template <class W, int LOGN, int LE, bool INV, bool PLO1, bool P2P, int TWM, int BF>
 __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaShape<W, LOGN, LE>::MINB)
     k_cols_tma(const __grid_constant__ CUtensorMap tmap, ColsParams prm, const TwPair<W>* __restrict__ tw,
-               const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, W p) {
+               const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb, const TwPair<W>* __restrict__ fm,
+               W p) {
   using Sh = ColsTmaShape<W, LOGN, LE>;
   extern __shared__ unsigned char smem_raw[];
   const uint32_t s0 = smem_u32(smem_raw);
@@ -153,7 +169,6 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
   auto bar_of = [&](int i) { return bar0 + (uint32_t)i * 8u; };
   const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
   const Mod<W> m = make_mod<W>(p);
-  const uint64_t cg_mask = (1ull << prm.log_colgroups) - 1;
   if (threadIdx.x == 0) {
     mbar_init(bar_of(0), 1);
     mbar_init(bar_of(1), 1);
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
   }
   __syncthreads();
   uint64_t tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE>(&tmap, tile, prm.log_colgroups, buf_of(0), bar_of(0));
+  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, tile, prm, buf_of(0), bar_of(0));
   W v[Sh::E];
   for (uint32_t it = 0; tile < prm.n_tiles; ++it, tile += gridDim.x) {
     const int cur = it & 1;
@@ -169,23 +184,25 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     if constexpr (Sh::R == 1) {  // no exchange to hide the prefetch behind: issue it now
       if (threadIdx.x == 0 && next < prm.n_tiles) {
         bulk_wait_read0();
-        cols_tma_issue<W, LOGN, LE>(&tmap, next, prm.log_colgroups, buf_of(cur ^ 1), bar_of(cur ^ 1));
+        cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, next, prm, buf_of(cur ^ 1), bar_of(cur ^ 1));
       }
     }
     mbar_wait(bar_of(cur), (it >> 1) & 1);
-    const uint32_t cglob = cols_global_column((uint32_t)((tile & cg_mask) * Sh::C + cc), prm);
+    uint64_t bq;
+    uint32_t cg;
+    cols_tile_coords<TWM == 2>(tile, prm, bq, cg);
+    const uint32_t cglob = cols_global_column(cg * Sh::C + cc, prm);
     W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, FACT, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, m, &tmap, next, buf_of(cur ^ 1),
-                                               bar_of(cur ^ 1), Sh::R > 1 && next < prm.n_tiles);
+    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, fm, m, &tmap, next,
+                                                    buf_of(cur ^ 1), bar_of(cur ^ 1), Sh::R > 1 && next < prm.n_tiles);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if constexpr (P2P) {
       // fused all-to-all: every 16-byte chunk of the tile goes straight to the receive buffer of
       // the rank that owns its row (peer memory over NVLink; the caller's cross-rank barrier
       // orders these stores before the row pass reads them)
-      const uint64_t bq = tile >> prm.log_colgroups;
-      const uint32_t c0 = (uint32_t)(tile & cg_mask) * Sh::C, rmask = (1u << prm.log_rows_rank) - 1;
+      const uint32_t c0 = cg * Sh::C, rmask = (1u << prm.log_rows_rank) - 1;
       constexpr int PER = 16 / (int)sizeof(W);
       for (int i = threadIdx.x; i < Sh::N * 8; i += Sh::THREADS) {
         const int row = i >> 3, k = i & 7;
@@ -201,10 +218,10 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
       // the loop, not behind a round's CTA barrier: every warp must have finished reading it first
       if constexpr (Sh::R == 1) __syncthreads();
     } else if (threadIdx.x == 0) {
-      const int bq = (int)(tile >> prm.log_colgroups), c0 = (int)(tile & cg_mask) * Sh::C;
+      const int c0 = (int)cg * Sh::C;
 #pragma unroll
       for (int bx = 0; bx < Sh::BOXES; ++bx)
-        tma_store_3d(&tmap, c0, bx * Sh::BOX_ROWS, bq, buf_of(cur) + bx * Sh::BOX_ROWS * 128);
+        tma_store_3d(&tmap, c0, bx * Sh::BOX_ROWS, (int)bq, buf_of(cur) + bx * Sh::BOX_ROWS * 128);
       bulk_commit();
     }
   }
@@ -224,7 +241,7 @@ template <class W, int LOGN> struct ColsTmaLE {
       sizeof(W) == 8 ? (LOGN == 9 ? NTT_COLS_LE64_9 : (LOGN < 4 ? LOGN : 4)) : (LOGN < 5 ? LOGN : 5);
 };
 
-template <class W, int LOGN, bool INV, bool PLO1, bool P2P, bool FACT>
+template <class W, int LOGN, bool INV, bool PLO1, bool P2P, int TWM, int BF = 3>
 static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
   constexpr int LE = ColsTmaLE<W, LOGN>::value;
   using Sh = ColsTmaShape<W, LOGN, LE>;
@@ -240,7 +257,7 @@ static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTable
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, FACT>;
+  auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, TWM, BF>;
   static PerDevice occ_cache;
   const int occ = occ_cache.get([&] {
     int o = 0;
@@ -253,14 +270,33 @@ static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTable
   if (!grid) return cudaSuccess;
   kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(map, prm, reinterpret_cast<const TwPair<W>*>(INV ? tb.sub_inv : tb.sub_fwd),
                                            reinterpret_cast<const TwPair<W>*>(tb.fa),
-                                           reinterpret_cast<const TwPair<W>*>(tb.fb), (W)p);
+                                           reinterpret_cast<const TwPair<W>*>(tb.fb),
+                                           reinterpret_cast<const TwPair<W>*>(tb.fm), (W)p);
   return cudaGetLastError();
 }
 
 template <class W, int LOGN, bool INV, bool PLO1, bool P2P>
 static cudaError_t run_cols_tma(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
-  if (prm.H) return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, true>(x, prm, tb, p, s);
-  return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, false>(x, prm, tb, p, s);
+  if constexpr (!INV && !P2P) {
+    // ablations F1 / F2 (forward column passes of Algorithm 2 / 5 plans): factored tables or the matrix
+    if (prm.bf == 2 || prm.bf == 5) {
+      if (!prm.matrix && !prm.H) return cudaErrorNotSupported;  // ablation plans never use direct tables
+      if constexpr (sizeof(W) == 8) {
+        if (prm.bf == 5) {
+          if constexpr (PLO1) return cudaErrorNotSupported;  // Algorithm 5 has no p-specific product
+          else return prm.matrix ? run_cols_tma_k<W, LOGN, INV, false, P2P, 2, 5>(x, prm, tb, p, s)
+                                 : run_cols_tma_k<W, LOGN, INV, false, P2P, 1, 5>(x, prm, tb, p, s);
+        }
+        return prm.matrix ? run_cols_tma_k<W, LOGN, INV, PLO1, P2P, 2, 2>(x, prm, tb, p, s)
+                          : run_cols_tma_k<W, LOGN, INV, PLO1, P2P, 1, 2>(x, prm, tb, p, s);
+      } else {
+        return cudaErrorNotSupported;  // beta = 2^32 multi-pass ablations: not built
+      }
+    }
+    if (prm.matrix && tb.fm) return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, 2>(x, prm, tb, p, s);
+  }
+  if (prm.H) return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, 1>(x, prm, tb, p, s);
+  return run_cols_tma_k<W, LOGN, INV, PLO1, P2P, 0>(x, prm, tb, p, s);
 }
 
 template <class W, bool INV, int LO, int HI>
@@ -272,7 +308,7 @@ static cudaError_t cols_tma_dispatch(int logn, void* x, const ColsParams& prm, c
     if (logn == LO) {
       // the fused all-to-all (p2p) epilogue is a separate instantiation, forward only
       if constexpr (sizeof(W) == 8) {
-        if ((p & 0xffffffffull) == 1) {
+        if ((p & 0xffffffffull) == 1 && prm.bf != 5) {
           if constexpr (!INV) {
             if (prm.p2p) return run_cols_tma<W, LO, INV, true, true>(x, prm, tb, p, s);
           }

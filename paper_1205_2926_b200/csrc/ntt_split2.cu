@@ -177,7 +177,7 @@ template <class W, int LOGQ, int LE> struct SplitFwd {
 // SCALE (forward with the pointwise product): stage 1 also multiplies by K = beta L^{-1} -- CTA 0's
 // sums by one Shoup product (work CTA 1 already spends on its twiddles), CTA 1's differences through
 // the pre-scaled table -- so the final product needs one REDC instead of REDC + Shoup.
-template <class W, int LOGQ, int LE, int LOGL, bool PLO1, bool UPPER, bool SCALE = false>
+template <class W, int LOGQ, int LE, int LOGL, bool PLO1, bool UPPER, bool SCALE = false, int BF = 3>
 __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const TwPair<W>* __restrict__ tw_full,
                                                  const Mod<W>& m, const SplitStage& st, const PwArgs& pw) {
   using F = SplitFwd<W, LOGQ, LE>;
@@ -194,16 +194,26 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
     for (int hh = 0; hh < F::HC; ++hh) {
       const int h = k * F::HC + hh, j = h * F::D + t;
       const W a = lo[hh * F::D + tsw], b = hi[hh * F::D + tsw];
+      NTT_AUDIT(a, BF == 2 ? m.p : m.p2);  // Alg. 3 / 5 input range (Alg. 2: canonical)
+      NTT_AUDIT(b, BF == 2 ? m.p : m.p2);
       if constexpr (!UPPER && SCALE) {
         v[h] = shoup_mul<W, PLO1>(a + b, (W)pw.K, (W)pw.Kp, m);  // a + b < 4p < beta: a Shoup input
       } else if constexpr (!UPPER) {
-        v[h] = csub<W>(a + b, m.p2);
+        v[h] = csub<W>(a + b, BF == 2 ? m.p : m.p2);  // Alg. 3/5 lines 1-2 (Alg. 2: canonical)
       } else {
         W w, wp;
         if constexpr (SCALE) ldtw<W>(reinterpret_cast<const TwPair<W>*>(pw.tw1s), (uint32_t)j, w, wp);
-        else ldtw<W>(tw_full, (uint32_t)(off + j), w, wp);
-        v[h] = shoup_mul<W, PLO1>(a - b + m.p2, w, wp, m);
+        else ldtw_bf<W, BF>(tw_full, (uint32_t)(off + j), w, wp);
+        if constexpr (BF == 2) v[h] = twiddle_mul<W, PLO1, 2>(a < b ? a - b + m.p : a - b, w, wp, m);  // Alg. 2
+        else if constexpr (BF == 5) v[h] = mont_mul<W>(a - b + m.p2, w, m);                           // Alg. 5
+        else {
+          W T = a - b + m.p2;
+          if (NTT_AUDIT_MUTATED()) T = a - b;
+          NTT_AUDIT(T, 2 * m.p2);  // Theorem 2: T in [0,4p)
+          v[h] = shoup_mul<W, PLO1>(T, w, wp, m);
+        }
       }
+      NTT_AUDIT(v[h], BF == 2 ? m.p : m.p2);
     }
     if (k == F::NX - 1) {  // X slots consumed: the late chunks reuse them
       fence_proxy_async_smem();
@@ -217,7 +227,7 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
 }
 
 
-template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW, int r>
+template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW, int BF, int r>
 __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int t, int rank,
                                             const TwPair<W>* __restrict__ tw_full, const Mod<W>& m,
                                             const PwArgs& pw, size_t boff, cg::cluster_group& cluster,
@@ -228,7 +238,10 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
   constexpr int S = 1 << SR, G = Sh::E >> SR;
   constexpr int D = Q >> (LEVEL + SR), B = Q >> LEVEL;
-  const TwPair<W>* tw_sub = tw_full + stage_off(LOGL, SS + 1);  // stages s+1..ell of the full per-stage table
+  // stages s+1..ell of the full per-stage table (Alg. 5 tables: one word per entry)
+  const TwPair<W>* tw_sub =
+      BF == 5 ? reinterpret_cast<const TwPair<W>*>(reinterpret_cast<const W*>(tw_full) + stage_off(LOGL, SS + 1))
+              : tw_full + stage_off(LOGL, SS + 1);
   constexpr bool REMAP = !INV && split_remap_last<LOGQ, LE, r>();  // this round: remapped groups
   int c[G], blk[G];
 #pragma unroll
@@ -245,14 +258,15 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       // the twiddled differences (lines 3-5, W = zeta_1^j).  The CTA-uniform choice is made outside
       // the element loops so the loads (data and twiddles) are scheduled ahead of their use.
       static_assert(G == 1 && S == SplitFwd<W, LOGQ, LE>::S, "first round: one column per thread");
-      if (rank == 0) split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, false, PW>(v, sm, t, tw_full, m, st, pw);
-      else split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, true, PW>(v, sm, t, tw_full, m, st, pw);
+      if (rank == 0) split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, false, PW, BF>(v, sm, t, tw_full, m, st, pw);
+      else split_fwd_stage1<W, LOGQ, LE, LOGL, PLO1, true, PW, BF>(v, sm, t, tw_full, m, st, pw);
       // every CTA has read x_b (the loaded values are consumed, so a relaxed arrive orders them):
       // arrive here, wait only before the last round's in-place store.  Measured against a full
       // cluster.sync() at this point: u32 2^16 -7%, u64 2^15 -3% (the wait no longer stalls the
       // early CTA, and cluster.sync's MEMBAR.GPU + L1 invalidate are gone).
       if constexpr (!PW) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     } else if constexpr (!INV) {
+      static_assert(BF == 3, "the K = 4 forward runs Algorithm 3 only");
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
@@ -359,7 +373,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         tma_load_2d(smem_u32(sm) + bx * F::BOXR * 128, st.map_a, 0, row0 + bx * F::BOXR, abar);
     }
   }
-  if constexpr (!INV) dif_round<W, LOGQ, SR, LEVEL, G, PLO1>(v, c, tw_sub, m);
+  if constexpr (!INV) dif_round<W, LOGQ, SR, LEVEL, G, PLO1, BF>(v, c, tw_sub, m);
   else dit_round<W, LOGQ, SR, LEVEL, G, PLO1>(v, c, tw_sub, m);
   if constexpr (last) {
     if constexpr (!INV) {
@@ -443,7 +457,6 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
             W u0[U], u1[U], w[U], wp[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const int j = (r0 ? 0 : PER_CTA) + (h0 + u) * D + t;
               const W theirs = sm[(h0 + u) * D + t];
               u0[u] = r0 ? mine_v[h0 + u] : theirs;  // x_j sits in CTA 0, x_{j+Q} in CTA 1
               u1[u] = r0 ? theirs : mine_v[h0 + u];
@@ -538,11 +551,11 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     if constexpr (WL) __syncwarp();
     else __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    split_round<W, LOGQ, LE, K, INV, PLO1, PW, nr>(v, xb, sm, t, rank, tw_full, m, pw, boff, cluster, st);
+    split_round<W, LOGQ, LE, K, INV, PLO1, PW, BF, nr>(v, xb, sm, t, rank, tw_full, m, pw, boff, cluster, st);
   }
 }
 
-template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW>
+template <class W, int LOGQ, int LE, int K, bool INV, bool PLO1, bool PW, int BF>
 __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
                                   SplitShape<LOGQ, LE, K, (int)sizeof(W)>::MINB)
     k_splitk(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_a, W* __restrict__ x,
@@ -598,7 +611,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
       }
     }
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    split_round<W, LOGQ, LE, K, INV, PLO1, PW, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster, st);
+    split_round<W, LOGQ, LE, K, INV, PLO1, PW, BF, r0>(v, x + boff, sm, t, rank, tw_full, m, pw, boff, cluster, st);
     if constexpr (INV) {
       // after the epilogue's cluster barrier no CTA reads this buffer any more
       fence_proxy_async_smem();
@@ -614,7 +627,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
 
 template <class W, int K> struct SplitLE { static constexpr int value = 5; };
 
-template <class W, int LOGL, int K, bool INV, bool PLO1, bool PW>
+template <class W, int LOGL, int K, bool INV, bool PLO1, bool PW, int BF = 3>
 static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, const PwArgs& pw, cudaStream_t s) {
   constexpr int LOGQ = LOGL - (K == 4 ? 2 : 1);
   constexpr int LE = SplitLE<W, K>::value;
@@ -642,7 +655,7 @@ static cudaError_t run_split(void* x, size_t batch, const void* tw, uint64_t p, 
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  auto kern = k_splitk<W, LOGQ, LE, K, INV, PLO1, PW>;
+  auto kern = k_splitk<W, LOGQ, LE, K, INV, PLO1, PW, BF>;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = K;
@@ -701,8 +714,23 @@ static cudaError_t run_split_k(void* x, size_t batch, const void* tw, uint64_t p
 
 cudaError_t launch_split2(int wbytes, int logn, bool inverse, void* x, size_t batch, const void* tw, uint64_t p,
                           const void* pw_a, const void* pw_b, uint64_t J, uint64_t K, uint64_t Kp, cudaStream_t s,
-                          const void* tw1s) {
+                          const void* tw1s, int bf) {
   PwArgs pw{pw_a, pw_b, J, K, Kp, tw1s};
+  if (bf != 3) {  // ablations F1 / F2: the plain forward on 2-CTA clusters (J for Algorithm 5)
+    if (inverse || pw_a || split_k() != 2 || (bf != 2 && bf != 5)) return cudaErrorNotSupported;
+    if (wbytes == 8) {
+      if (logn != kContigMaxLog64 + 1) return cudaErrorInvalidValue;
+      constexpr int L = kContigMaxLog64 + 1;
+      const bool plo1 = (p & 0xffffffffull) == 1;
+      if (bf == 5) return run_split<uint64_t, L, 2, false, false, false, 5>(x, batch, tw, p, pw, s);
+      return plo1 ? run_split<uint64_t, L, 2, false, true, false, 2>(x, batch, tw, p, pw, s)
+                  : run_split<uint64_t, L, 2, false, false, false, 2>(x, batch, tw, p, pw, s);
+    }
+    if (logn != kContigMaxLog32 + 1) return cudaErrorInvalidValue;
+    constexpr int L = kContigMaxLog32 + 1;
+    if (bf == 5) return run_split<uint32_t, L, 2, false, false, false, 5>(x, batch, tw, p, pw, s);
+    return run_split<uint32_t, L, 2, false, false, false, 2>(x, batch, tw, p, pw, s);
+  }
   // fused (pw_a set): inverse -- a <- InvNTT(a * b L^{-1}); forward -- a <- NTT(x) * a L^{-1}, x only
   // read (K = 2 only)
   const bool fused = pw_a != nullptr;

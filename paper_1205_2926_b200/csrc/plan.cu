@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/ntt_b200.h"
@@ -82,37 +83,73 @@ std::vector<uint8_t> make_table(uint64_t p, uint64_t root, uint64_t count, unsig
 
 }  // namespace
 
-// Per-stage table of an N = 2^logn point transform with root `root` (rounds.cuh):
-// stage i (1-based) holds zeta_i^k = root^{2^{i-1} k}, k < N >> i, at offset N - (N >> (i-1)).
-// The first N/2 entries (stage 1) are root^e, e < N/2.
+// Per-stage table of an N = 2^logn point transform with root `root` (rounds.cuh stage_off):
+// stage i (1-based) holds zeta_i^k = root^{2^{i-1} k}, k <= m_i = N >> i, at offset
+// N - (N >> (i-1)) + (i-1).  The first N/2 entries (stage 1) are root^e, e < N/2.  The extra entry
+// k = m_i (= -1) lets the inverse read zeta_i^{-k} = -zeta_i^{m_i - k} from this same table
+// (rounds.cuh inv_index), so no inverse table is built.
 std::vector<uint8_t> make_stage_table(uint64_t p, uint64_t root, unsigned logn, unsigned bits) {
   const uint64_t N = (uint64_t)1 << logn;
   std::vector<uint8_t> out;
   if (logn == 0) return out;
-  out.reserve((N - 1) * 2 * (bits / 8));
+  out.reserve((N - 1 + logn) * 2 * (bits / 8));
   uint64_t zeta = root;
   for (unsigned i = 1; i <= logn; ++i) {
-    std::vector<uint8_t> t = make_table(p, zeta, N >> i, bits);
+    std::vector<uint8_t> t = make_table(p, zeta, (N >> i) + 1, bits);
     out.insert(out.end(), t.begin(), t.end());
     zeta = mulmod(zeta, zeta, p);
   }
   return out;
 }
 
-// Algorithm 5 variant of the per-stage table: first word W'_mont = beta * W mod p,
-// second word unused.
-std::vector<uint8_t> make_stage_table_mont(uint64_t p, uint64_t root, unsigned logn, unsigned bits) {
-  std::vector<uint8_t> t = make_stage_table(p, root, logn, bits);
-  const size_t wb = bits / 8, n = t.size() / (2 * wb);
+// Algorithm 5 form of a table of (W, W') pairs: one word per entry, W'_mont = beta W mod p (P:174,
+// "only a single value W' must be stored") -- half the bytes of the Shoup pairs.
+std::vector<uint8_t> to_mont_words(const std::vector<uint8_t>& pairs, uint64_t p, unsigned bits) {
+  const size_t wb = bits / 8, n = pairs.size() / (2 * wb);
   const uint64_t bmodp = (uint64_t)(((u128)1 << bits) % p);
+  std::vector<uint8_t> out(n * wb);
   for (size_t e = 0; e < n; ++e) {
     uint64_t w = 0;
-    memcpy(&w, &t[2 * e * wb], wb);
-    const uint64_t wm = mulmod(w, bmodp, p), zero = 0;
-    memcpy(&t[2 * e * wb], &wm, wb);
-    memcpy(&t[(2 * e + 1) * wb], &zero, wb);
+    memcpy(&w, &pairs[2 * e * wb], wb);
+    const uint64_t wm = mulmod(w, bmodp, p);
+    memcpy(&out[e * wb], &wm, wb);
   }
-  return t;
+  return out;
+}
+
+// Algorithm 5 variant of the per-stage table (same layout, one word per entry).
+std::vector<uint8_t> make_stage_table_mont(uint64_t p, uint64_t root, unsigned logn, unsigned bits) {
+  return to_mont_words(make_stage_table(p, root, logn, bits), p, bits);
+}
+
+// Four-step twiddle matrix of a column pass: N = 2^logn rows x S = 2^logs columns,
+// row-major, entry (r, c) = (W, W') of W = rootB^{c rev_logn(r)} (rootB = omega_B, B = N S).  Built by
+// rows on the host's cores: row r is the geometric sequence of rootB^{rev(r)}.
+std::vector<uint8_t> make_fourstep_matrix(uint64_t p, uint64_t rootB, unsigned logn, unsigned logs, unsigned bits) {
+  const uint64_t N = (uint64_t)1 << logn, S = (uint64_t)1 << logs;
+  const size_t wb = bits / 8;
+  std::vector<uint8_t> out(N * S * 2 * wb);
+  auto rows = [&](uint64_t r0, uint64_t r1) {
+    for (uint64_t r = r0; r < r1; ++r) {
+      uint64_t rv = 0;
+      for (unsigned b = 0; b < logn; ++b) rv |= ((r >> b) & 1) << (logn - 1 - b);
+      const uint64_t base = powmod(rootB, rv, p);
+      uint64_t w = 1;
+      uint8_t* dst = &out[r * S * 2 * wb];
+      for (uint64_t c = 0; c < S; ++c) {
+        const uint64_t wp = (uint64_t)(((u128)w << bits) / p);
+        memcpy(dst + (2 * c) * wb, &w, wb);  // little-endian: the low wb bytes
+        memcpy(dst + (2 * c + 1) * wb, &wp, wb);
+        w = mulmod(w, base, p);
+      }
+    }
+  };
+  unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (N * S < ((uint64_t)1 << 16)) nt = 1;
+  std::vector<std::thread> th;
+  for (unsigned i = 0; i < nt; ++i) th.emplace_back(rows, N * i / nt, N * (i + 1) / nt);
+  for (auto& t : th) t.join();
+  return out;
 }
 
 bool tma_enabled() {
@@ -134,16 +171,18 @@ struct ntt_plan_s {
   // device tables
   void* tw_fwd = nullptr;  // single pass: omega^e, e < L/2
   void* tw1s = nullptr;    // cluster sizes: stage-1 entries omega^e K_scale, e < L/2 (fused convolution)
-  void* tw_inv = nullptr;  // single pass: omega^{-e}
-  std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables
+  void* tw_inv = nullptr;  // single pass, read by the inverse (negated entries): tw_fwd itself, or for
+                           // Algorithm 5 plans (Montgomery tw_fwd) the Shoup table of omega
+  std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables (sub_inv[j] == sub_fwd[j])
   std::vector<void*> owned;
   // lazily built tables for the distributed four-step entry points (guarded by mu)
   std::mutex mu;
-  std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e table
-  std::map<unsigned, void*> extra_sub_inv;  // log2 N -> omega_N^{-e} table
+  std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e per-stage table (forward and inverse)
   // four-step twiddle tables per block level: log2 B -> (table A, table B, H) for omega_B^e, e < B
   struct FsTables { void* fa; void* fb; unsigned H; };
   std::map<unsigned, FsTables> fs_level;
+  std::map<unsigned, void*> fs_matrix;  // (bf << 16 | log2 B << 8 | log2 N) -> forward twiddle matrix of that pass
+  std::map<unsigned, FsTables> fs_level_bf;  // ablation plans' forward four-step factors (bf << 8 | log2 B)
   // host-buffer executor (ntt_execute_host): pipeline streams and events
   static constexpr int kRing = 8;           // max device buffers in the host pipeline's ring
   static constexpr int kDefaultRing = 4;
@@ -250,16 +289,17 @@ std::vector<unsigned> make_schedule(unsigned ell, unsigned wbytes) {
   }
 }
 
-// Per-stage table of omega_N (inverse: omega_N^{-1}) for N = 2^logn, built once per plan
-// (distributed entry points).
+// Per-stage table of omega_N for N = 2^logn, built once per plan (distributed entry points); the
+// inverse kernels read the same table (negated entries, rounds.cuh inv_index).
 ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out, bool inverse = false) {
+  (void)inverse;
   std::lock_guard<std::mutex> lk(pl->mu);
-  auto& cache = inverse ? pl->extra_sub_inv : pl->extra_sub;
+  auto& cache = pl->extra_sub;
   auto it = cache.find(logn);
   if (it != cache.end()) { *out = it->second; return NTT_OK; }
   const uint64_t L = (uint64_t)1 << pl->ell, Nn = (uint64_t)1 << logn;
   void* d = nullptr;
-  const uint64_t root = powmod(inverse ? pl->omega_inv : pl->omega, L / Nn, pl->p);
+  const uint64_t root = powmod(pl->omega, L / Nn, pl->p);
   ntt_status st = upload(pl, make_stage_table(pl->p, root, logn, pl->bits), &d);
   if (st != NTT_OK) return st;
   cache[logn] = d;
@@ -274,10 +314,16 @@ ntt_status sub_table(ntt_plan_s* pl, unsigned logn, void** out, bool inverse = f
 // omega_B^{e & (2^H - 1)} (two Shoup multiplies) with H = min(ceil(lb / 2), 10): the low factor
 // (indexed by e mod 2^H, scattered across a warp) stays in L1, the high one (indexed by e >> H,
 // nearly uniform across neighbouring columns) in L2.  Measured C5: H = 14 6.37 ms, H = 10 6.06 ms.
-ntt_status fourstep_level_tables(ntt_plan_s* pl, unsigned lb, ntt_plan_s::FsTables* out) {
+// bf = 2 / 5 (forward column passes of the ablation plans, F1 / F2): always factored (H >= 1; the
+// ablation kernels have no direct-table form), Shoup pairs for Algorithm 2, one-word Montgomery
+// factors for Algorithm 5 (its twiddle product is Alg. 5's multiply).
+ntt_status fourstep_level_tables(ntt_plan_s* pl, unsigned lb, ntt_plan_s::FsTables* out, unsigned bf = 3) {
   std::lock_guard<std::mutex> lk(pl->mu);
-  auto it = pl->fs_level.find(lb);
-  if (it != pl->fs_level.end()) { *out = it->second; return NTT_OK; }
+  auto& cache = bf == 3 ? pl->fs_level : pl->fs_level_bf;
+  const unsigned key = bf == 3 ? lb : ((bf << 8) | lb);
+  auto it = cache.find(key);
+  if (it != cache.end()) { *out = it->second; return NTT_OK; }
+  auto form = [&](std::vector<uint8_t> pairs) { return bf == 5 ? to_mont_words(pairs, pl->p, pl->bits) : pairs; };
   const uint64_t B = (uint64_t)1 << lb;
   const uint64_t root = powmod(pl->omega, ((uint64_t)1 << pl->ell) >> lb, pl->p);
   ntt_plan_s::FsTables t{nullptr, nullptr, 0};
@@ -288,7 +334,7 @@ ntt_status fourstep_level_tables(ntt_plan_s* pl, unsigned lb, ntt_plan_s::FsTabl
     const char* e = getenv("NTT_FS_DIRECT_MAX");
     return e ? (unsigned)atoi(e) : 16u;
   }();
-  if (lb <= direct_max) {
+  if (lb <= direct_max && bf == 3) {
     st = upload(pl, make_table(pl->p, root, B, pl->bits), &t.fa);
     t.fb = t.fa;
   } else {
@@ -297,13 +343,52 @@ ntt_status fourstep_level_tables(ntt_plan_s* pl, unsigned lb, ntt_plan_s::FsTabl
       const unsigned h = (unsigned)atoi(e);
       if (h >= 1 && h < lb) t.H = h;
     }
-    st = upload(pl, make_table(pl->p, powmod(root, (uint64_t)1 << t.H, pl->p), B >> t.H, pl->bits), &t.fa);
-    if (st == NTT_OK) st = upload(pl, make_table(pl->p, root, (uint64_t)1 << t.H, pl->bits), &t.fb);
+    st = upload(pl, form(make_table(pl->p, powmod(root, (uint64_t)1 << t.H, pl->p), B >> t.H, pl->bits)), &t.fa);
+    if (st == NTT_OK) st = upload(pl, form(make_table(pl->p, root, (uint64_t)1 << t.H, pl->bits)), &t.fb);
   }
   if (st != NTT_OK) return st;
-  pl->fs_level[lb] = t;
+  cache[key] = t;
   *out = t;
   return NTT_OK;
+}
+
+// Largest block level with a forward twiddle matrix (env NTT_FS_MATRIX_MAX, default 24: C4's 2^24 level
+// takes 256 MiB; C5's 2^28 level would take 4 GiB and keeps the factored tables).
+unsigned fs_matrix_max() {
+  static const unsigned v = [] {
+    const char* e = getenv("NTT_FS_MATRIX_MAX");
+    return e ? (unsigned)atoi(e) : 24u;
+  }();
+  return v;
+}
+
+// Forward twiddle matrix of the column pass with blocks of 2^lb words and 2^logn rows (nullptr when
+// the level uses a direct table or exceeds fs_matrix_max()).
+ntt_status fourstep_matrix(ntt_plan_s* pl, unsigned lb, unsigned logn, void** out, unsigned bf = 3) {
+  *out = nullptr;
+  static const unsigned direct_max = [] {
+    const char* e = getenv("NTT_FS_DIRECT_MAX");
+    return e ? (unsigned)atoi(e) : 16u;
+  }();
+  if (lb <= direct_max || lb > fs_matrix_max() || logn >= lb) return NTT_OK;
+  std::lock_guard<std::mutex> lk(pl->mu);
+  const unsigned key = (bf << 16) | (lb << 8) | logn;
+  auto it = pl->fs_matrix.find(key);
+  if (it != pl->fs_matrix.end()) { *out = it->second; return NTT_OK; }
+  const uint64_t rootB = powmod(pl->omega, ((uint64_t)1 << pl->ell) >> lb, pl->p);
+  void* d = nullptr;
+  std::vector<uint8_t> mat = make_fourstep_matrix(pl->p, rootB, logn, lb - logn, pl->bits);
+  if (bf == 5) mat = to_mont_words(mat, pl->p, pl->bits);  // Algorithm 5: one word per entry
+  ntt_status st = upload(pl, mat, &d);
+  if (st != NTT_OK) return st;
+  pl->fs_matrix[key] = d;
+  *out = d;
+  return NTT_OK;
+}
+
+unsigned env_uint(const char* name, unsigned dflt) {
+  const char* e = getenv(name);
+  return e ? (unsigned)atoi(e) : dflt;
 }
 
 }  // namespace
@@ -385,8 +470,14 @@ ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsig
   if (pl->passes.size() == 1) {
     if ((st = upload(pl, butterfly == NTT_BFLY_ALG5 ? make_stage_table_mont(p, omega, ell, bits)
                                                     : make_stage_table(p, omega, ell, bits),
-                     &pl->tw_fwd)) != NTT_OK ||
-        (st = upload(pl, make_stage_table(p, pl->omega_inv, ell, bits), &pl->tw_inv)) != NTT_OK) {
+                     &pl->tw_fwd)) != NTT_OK) {
+      free_plan(pl);
+      return st;
+    }
+    // the inverse (Algorithm 4, Shoup pairs) reads the forward table's negated entries
+    pl->tw_inv = pl->tw_fwd;
+    if (butterfly == NTT_BFLY_ALG5 &&
+        (st = upload(pl, make_stage_table(p, omega, ell, bits), &pl->tw_inv)) != NTT_OK) {
       free_plan(pl);
       return st;
     }
@@ -398,20 +489,26 @@ ntt_status ntt_plan_create_ex(ntt_plan_t* out, uint64_t p, uint64_t omega, unsig
   } else {
     for (unsigned n : pl->passes) {
       const uint64_t Nn = (uint64_t)1 << n;
-      const uint64_t rootN = powmod(omega, L / Nn, p), rootNi = powmod(pl->omega_inv, L / Nn, p);
-      void *f = nullptr, *i = nullptr;
-      if ((st = upload(pl, make_stage_table(p, rootN, n, bits), &f)) != NTT_OK ||
-          (st = upload(pl, make_stage_table(p, rootNi, n, bits), &i)) != NTT_OK) {
+      const uint64_t rootN = powmod(omega, L / Nn, p);
+      void *f = nullptr, *fi = nullptr;
+      if ((st = upload(pl, make_stage_table(p, rootN, n, bits), &fi)) != NTT_OK ||
+          (butterfly == NTT_BFLY_ALG5 && (st = upload(pl, make_stage_table_mont(p, rootN, n, bits), &f)) != NTT_OK)) {
         free_plan(pl);
         return st;
       }
-      pl->sub_fwd.push_back(f);
-      pl->sub_inv.push_back(i);
+      pl->sub_fwd.push_back(butterfly == NTT_BFLY_ALG5 ? f : fi);
+      pl->sub_inv.push_back(fi);  // the inverse reads the Shoup table (negated entries)
     }
     unsigned outer = 0;
     for (size_t j = 0; j + 1 < pl->passes.size(); ++j) {
       ntt_plan_s::FsTables t;
-      if ((st = fourstep_level_tables(pl, ell - outer, &t)) != NTT_OK) { free_plan(pl); return st; }
+      void* fm = nullptr;
+      if ((st = fourstep_level_tables(pl, ell - outer, &t)) != NTT_OK ||
+          (butterfly != NTT_BFLY_ALG3 && (st = fourstep_level_tables(pl, ell - outer, &t, butterfly)) != NTT_OK) ||
+          (st = fourstep_matrix(pl, ell - outer, pl->passes[j], &fm, butterfly)) != NTT_OK) {
+        free_plan(pl);
+        return st;
+      }
       outer += pl->passes[j];
     }
   }
@@ -490,6 +587,19 @@ static cudaError_t launch_cols_any(int wbytes, int logn, bool inverse, void* x, 
 
 static std::atomic<unsigned> g_range_checks{0};
 
+#ifdef NTT_RANGE_AUDIT
+// Range-audit build: every translation unit with kernels registers its counter accessors
+// (modarith.cuh); a function-local static so registration from other TUs' static initialisers is
+// safe regardless of initialisation order.
+static std::vector<nttb::AuditTU>& audit_tus() {
+  static std::vector<nttb::AuditTU> v;
+  return v;
+}
+}  // extern "C"
+void nttb::audit_register(const nttb::AuditTU& tu) { audit_tus().push_back(tu); }
+extern "C" {
+#endif
+
 // Range-checking mode: scan x for words >= bound; NTT_ERR_RANGE on a violation.
 static ntt_status check_range(ntt_plan_t pl, const void* x, size_t n, uint64_t bound, cudaStream_t s) {
   unsigned* flag = nullptr;
@@ -512,9 +622,17 @@ static cudaError_t run_pass(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s
   const unsigned np = (unsigned)pl->passes.size();
   if (pl->ell == 0)  // identity; only the normalisation remains
     return nttb::launch_normalize(pl->wbytes, x, batch, pl->p, inverse ? 1 : 0, s);
-  if (pl->bfly != NTT_BFLY_ALG3 && !inverse)  // F1/F2 ablation: on-chip TMA kernel only
-    return nttb::launch_contig_tma(pl->wbytes, (int)pl->ell, false, true, x, batch, pl->tw_fwd, pl->p, s,
-                                   (int)pl->bfly);
+  const bool abl = pl->bfly != NTT_BFLY_ALG3 && !inverse;  // F1/F2 ablation forward: BF-templated kernels only
+  if (abl && (np == 1 || j + 1 == np)) {
+    const unsigned n = np == 1 ? pl->ell : pl->passes[np - 1];
+    const size_t rows = np == 1 ? batch : batch * (L >> n);
+    const void* tw = np == 1 ? pl->tw_fwd : pl->sub_fwd[np - 1];
+    if (nttb::split2_supported(pl->wbytes, (int)n))
+      return nttb::launch_split2(pl->wbytes, (int)n, false, x, rows, tw, pl->p, nullptr, nullptr, 0, 0, 0, s,
+                                 nullptr, (int)pl->bfly);
+    if (!nttb::tma_supported(pl->wbytes, (int)n)) return cudaErrorNotSupported;
+    return nttb::launch_contig_tma(pl->wbytes, (int)n, false, true, x, rows, tw, pl->p, s, (int)pl->bfly);
+  }
   if (np == 1)
     return launch_contig_any(pl->wbytes, (int)pl->ell, inverse, true, x, batch, inverse ? pl->tw_inv : pl->tw_fwd,
                              pl->p, s);
@@ -542,8 +660,28 @@ static cudaError_t run_pass(ntt_plan_t pl, void* x, size_t batch, cudaStream_t s
   ntt_plan_s::FsTables t{};
   if (fourstep_level_tables(pl, prm.ell, &t) != NTT_OK)  // built at plan creation: a cache hit
     return cudaErrorMemoryAllocation;
+  if (abl && fourstep_level_tables(pl, prm.ell, &t, pl->bfly) != NTT_OK) return cudaErrorMemoryAllocation;
   prm.H = t.H;
+  prm.bf = inverse ? 3 : pl->bfly;
   nttb::DevTables tb{pl->sub_fwd[j], pl->sub_inv[j], t.fa, t.fb};
+  if (!inverse) {
+    void* fm = nullptr;
+    if (fourstep_matrix(pl, logB, logN, &fm, pl->bfly) != NTT_OK) return cudaErrorMemoryAllocation;  // cache hit
+    if (fm) {
+      tb.fm = fm;
+      prm.matrix = 1;
+      // blocks fastest within runs of 2^log_cgi column groups: the CTAs in flight read the same few
+      // column groups' matrix rows (L2-resident) for every transform of the batch
+      static const unsigned bmajor = env_uint("NTT_COLS_BMAJOR", 1), cgi = env_uint("NTT_COLS_CGI", 2);
+      const unsigned groups_log = prm.log_colgroups;
+      prm.bmajor = bmajor;
+      prm.log_cgi = std::min(cgi, groups_log);
+    }
+  }
+  if (abl) {  // the ablation butterflies exist in the TMA-staged column kernel only (no fallback)
+    if (!nttb::cols_tma_supported(pl->wbytes, (int)pl->passes[j], prm, x)) return cudaErrorNotSupported;
+    return nttb::launch_cols_tma(pl->wbytes, (int)pl->passes[j], false, x, prm, tb, pl->p, s);
+  }
   return launch_cols_any(pl->wbytes, (int)pl->passes[j], inverse, x, prm, tb, pl->p, s);
 }
 
@@ -567,14 +705,15 @@ static ntt_status run_transform(ntt_plan_t pl, void* x, size_t batch, cudaStream
     ntt_status st = check_range(pl, x, batch * L, bound, s);
     if (st != NTT_OK) return st;
   }
-  const unsigned np = (pl->ell == 0 || (pl->bfly != NTT_BFLY_ALG3 && !inverse)) ? 1u : (unsigned)pl->passes.size();
-  if (np > 1 && pl->bfly != NTT_BFLY_ALG3 && !inverse) return NTT_ERR_UNSUPPORTED;
-  if (pl->bfly != NTT_BFLY_ALG3 && !inverse && !nttb::tma_supported((int)pl->wbytes, (int)pl->ell))
-    return NTT_ERR_UNSUPPORTED;
+  const unsigned np = pl->ell == 0 ? 1u : (unsigned)pl->passes.size();
   cudaError_t e = cudaSuccess;
   for (unsigned k = 0; k < np && e == cudaSuccess; ++k) {
     e = run_pass(pl, x, batch, s, inverse, inverse ? np - 1 - k : k);
     ++t_launches;
+  }
+  if (e == cudaErrorNotSupported) {  // a size the ablation kernels do not cover (before any launch)
+    cudaGetLastError();
+    return NTT_ERR_UNSUPPORTED;
   }
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
@@ -676,6 +815,48 @@ ntt_status ntt_execute_host(ntt_plan_t pl, unsigned ops, const void* host_in, vo
 
 unsigned ntt_set_range_checks(unsigned on) { return g_range_checks.exchange(on ? 1u : 0u); }
 
+unsigned ntt_build_flags(void) {
+#ifdef NTT_RANGE_AUDIT
+  return NTT_BUILD_RANGE_AUDIT;
+#else
+  return 0;
+#endif
+}
+
+ntt_status ntt_audit_counts(int device, uint64_t* violations) {
+  if (!violations) return NTT_ERR_ARG;
+  *violations = 0;
+#ifdef NTT_RANGE_AUDIT
+  DeviceGuard g(device);
+  if (!g.ok) return cuda_fail(cudaGetLastError());
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (const auto& tu : audit_tus()) *violations += tu.read();
+  return NTT_OK;
+#else
+  (void)device;
+  return NTT_ERR_UNSUPPORTED;
+#endif
+}
+
+ntt_status ntt_audit_reset(int device, int mutate) {
+#ifdef NTT_RANGE_AUDIT
+  DeviceGuard g(device);
+  if (!g.ok) return cuda_fail(cudaGetLastError());
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (const auto& tu : audit_tus()) {
+    tu.reset();
+    tu.mutate(mutate ? 1 : 0);
+  }
+  return NTT_OK;
+#else
+  (void)device;
+  (void)mutate;
+  return NTT_ERR_UNSUPPORTED;
+#endif
+}
+
 ntt_status ntt_forward(ntt_plan_t plan, void* x, size_t batch, ntt_stream_t stream) {
   return run_transform(plan, x, batch, (cudaStream_t)stream, false);
 }
@@ -689,12 +870,15 @@ ntt_status ntt_transform_pass(ntt_plan_t pl, void* x, size_t batch, unsigned inv
   t_launches = 0;
   if (ntt_status st = check_transform_args(pl, x, batch); st != NTT_OK) return st;
   if (inverse > 1 || pass >= pl->passes.size()) return NTT_ERR_ARG;
-  if (pl->bfly != NTT_BFLY_ALG3 && !inverse && pl->passes.size() > 1) return NTT_ERR_UNSUPPORTED;
   if (!batch) return NTT_OK;
   DeviceGuard g(pl->device);
   if (!g.ok) return cuda_fail(cudaGetLastError());
   cudaError_t e = run_pass(pl, x, batch, (cudaStream_t)stream, inverse != 0, pass);
   ++t_launches;
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return NTT_ERR_UNSUPPORTED;
+  }
   return e == cudaSuccess ? NTT_OK : cuda_fail(e);
 }
 

@@ -31,6 +31,18 @@ template <> __device__ __forceinline__ void ldtw<uint32_t>(const TwPair<uint32_t
   wp = t.y;
 }
 
+// Twiddle load for forward butterfly BF: (W, W') pairs, or for Algorithm 5 the single word
+// beta W mod p ("only a single value W' must be stored") -- its tables hold one word per entry.
+template <class W, int BF>
+__device__ __forceinline__ void ldtw_bf(const TwPair<W>* tw, uint32_t e, W& w, W& wp) {
+  if constexpr (BF == 5) {
+    w = __ldg(reinterpret_cast<const W*>(tw) + e);
+    wp = 0;
+  } else {
+    ldtw<W>(tw, e, w, wp);
+  }
+}
+
 // Offset of stage i's table inside the per-stage layout of an N-point transform: stage i holds
 // zeta_i^k for k <= m_i = N >> i (m_i + 1 entries; the last one is zeta_i^{m_i} = omega^{N/2} = -1).
 __host__ __device__ constexpr int stage_off(int logn, int i) {
@@ -74,7 +86,7 @@ template <int LOGN, int LE, int ra, int rb> __host__ __device__ constexpr bool w
 // every k = 0 butterfly of a round with D = 1) take the multiply-free path.
 // BF selects the butterfly: 3 = Algorithm 3 (the product path), 2 = Algorithm 2 and
 // 5 = Algorithm 5 (ablations F1/F2 of SURVEY.md §8(f); Alg. 5 reads W' = beta W mod p
-// from the first word of each table pair).
+// from a one-word-per-entry table, ldtw_bf).
 template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
   constexpr int S = 1 << SR;
@@ -91,20 +103,12 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
         // k = hh*D + c; when D == 1 (c == 0) the hh == 0 butterflies have k = 0, i.e. W = 1
         const bool unit = w1 || (D == 1 && hh == 0);
         W w = 1, wp = 0;
-        if (!unit) ldtw<W>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
+        if (!unit) ldtw_bf<W, BF>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if constexpr (BF == 2) {
-            if (unit) bfly_alg2_w1<W>(v[q * S + h], v[q * S + h + half], m.p);
-            else bfly_alg2m<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
-          } else if constexpr (BF == 5) {
-            if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
-            else bfly_alg5m<W>(v[q * S + h], v[q * S + h + half], w, m);
-          } else {
-            if (unit) bfly_alg3_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
-            else bfly_alg3<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
-          }
+          if (unit) bfly_fwd_w1<W, BF>(v[q * S + h], v[q * S + h + half], m);
+          else bfly_fwd<W, PLO1, BF>(v[q * S + h], v[q * S + h + half], w, wp, m);
         }
       }
     }

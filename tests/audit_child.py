@@ -1,0 +1,85 @@
+"""Child process of test_gpu_audit.py: loads the range-audit build (NTT_B200_LIB=audit) and runs the
+config shapes through it, printing one JSON object of violation counts per case."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1205_2926_b200 as ntt  # noqa: E402
+import synth  # noqa: E402
+
+P30, P62 = 998244353, 29 * 2**57 + 1
+
+
+def root(p, L):
+    return pow(3, (p - 1) // L, p)
+
+
+def case(name, fn, mutate=False):
+    ntt.audit_reset(0, mutate=mutate)
+    fn()
+    torch.cuda.synchronize()
+    out[name] = ntt.audit_counts(0)
+    ntt.audit_reset(0, mutate=False)
+
+
+def transform(p, bits, ell, batch, ops=("fwd", "inv"), alg=3, top=False):
+    def fn():
+        L = 1 << ell
+        plan = ntt.Plan(p, root(p, L), ell, bits, butterfly=alg)
+        dt = torch.uint64 if bits == 64 else torch.uint32
+        x = torch.empty(batch * L, dtype=dt, device="cuda")
+        ntt.synth_uniform(x, synth.config_seed(7), ell, bound=p)
+        def fill(v):  # word v in every 3rd / 5th place (through a signed view: torch has no uint64 fill)
+            if bits == 64:
+                return x.view(torch.int64), v - (1 << 64) if v >= 1 << 63 else v
+            return x.view(torch.int32), v - (1 << 32) if v >= 1 << 31 else v
+        if top:  # inputs at the top of Algorithm 3's accepted range [0,2p)
+            t, v = fill(2 * p - 1)
+            t[::3] = v
+        for op in ops:
+            if op == "inv" and top:
+                t, v = fill(4 * p - 1)  # Algorithm 4 accepts [0,4p)
+                t[::5] = v
+            (plan.forward if op == "fwd" else plan.inverse)(x)
+    return fn
+
+
+def conv(batch):
+    def fn():
+        L = 1 << 16
+        for p in (469762049, 167772161, 998244353):
+            plan = ntt.Plan(p, root(p, L), 16, 32)
+            a = torch.zeros(batch, L, dtype=torch.uint32, device="cuda")
+            b = torch.zeros_like(a)
+            t = torch.empty(batch * L // 2, dtype=torch.uint32, device="cuda")
+            ntt.synth_uniform(t, 3, 0, bits=20)
+            a[:, :L // 2] = t.view(batch, -1)
+            ntt.synth_uniform(t, 3, 1, bits=20)
+            b[:, :L // 2] = t.view(batch, -1)
+            plan.cyclic_convolve(a, b)
+    return fn
+
+
+assert ntt.audit_build(), "NTT_B200_LIB=audit did not load the audit build"
+out = {}
+which = sys.argv[1:] or ["all"]
+if "all" in which or "clean" in which:
+    case("C1 2^10 u32", transform(P30, 32, 10, 1, top=True))
+    case("C2 4096 x 2^12 u64 fwd+inv", transform(P62, 64, 12, 4096, top=True))
+    case("C3 64 pairs x 2^16 u32 convolution (3 primes)", conv(64))
+    case("2^15 u64 cluster fwd+inv", transform(P62, 64, 15, 64, top=True))
+    case("C4 shape 2 x 2^24 u64 fwd+inv", transform(P62, 64, 24, 2, top=True))
+    case("C5 shape 2^28 u64 fwd+inv", transform(P62, 64, 28, 1, top=True))
+    case("C4 shape 2 x 2^24 u64 fwd Alg. 5", transform(P62, 64, 24, 2, ops=("fwd",), alg=5))
+    case("C4 shape 2 x 2^24 u64 fwd Alg. 2", transform(P62, 64, 24, 2, ops=("fwd",), alg=2))
+    case("2^20 u32 fwd+inv", transform(P30, 32, 20, 2, top=True))
+if "all" in which or "mutant" in which:
+    case("MUTANT C2 4096 x 2^12 u64 fwd", transform(P62, 64, 12, 4096, ops=("fwd",)), mutate=True)
+    case("MUTANT C4 shape 1 x 2^24 u64 fwd", transform(P62, 64, 24, 1, ops=("fwd",)), mutate=True)
+    case("MUTANT 2^16 u32 fwd", transform(P30, 32, 16, 8, ops=("fwd",)), mutate=True)
+print(json.dumps(out))

@@ -109,3 +109,19 @@ def test_fourstep_entry_points_reject_null_plan(ntt):
     lib = ntt.lib()
     assert lib.ntt_fourstep_cols_inv(None, 7, None, 0, 2, None) == -1
     assert lib.ntt_fourstep_rows_inv(None, 7, None, None, 0, 2, None) == -1
+
+
+def test_audit_build_exports_and_production_refuses(ntt):
+    """The range-audit debug build exports the same ABI; the production build has no audit counters."""
+    audit = os.path.join(ROOT, "paper_1205_2926_b200", "libntt_b200_audit.so")
+    assert os.path.exists(audit)
+    lib = ctypes.CDLL(audit)
+    for n in header_functions():
+        assert hasattr(lib, n), n
+    lib.ntt_build_flags.restype = ctypes.c_uint
+    assert lib.ntt_build_flags() & 1
+    prod = ntt.lib()
+    assert prod.ntt_build_flags() == 0
+    v = ctypes.c_uint64(7)
+    assert prod.ntt_audit_counts(0, ctypes.byref(v)) == -8 and v.value == 0
+    assert prod.ntt_audit_reset(0, 0) == -8

@@ -1,5 +1,7 @@
 """The paper's Table 1 comparison (Algorithm 2 vs Algorithm 3, cycles per butterfly,
-L = 2^11, 62-bit prime) re-run on B200 with batched on-chip transforms; Algorithm 5 added (F2).
+L = 2^11, 62-bit prime) re-run on B200 with batched transforms; Algorithm 5 added (F2).  Besides the
+paper's shape, one line per BASELINE config (C1-C5 forward), each running the config's own kernels
+(on-chip, 2-CTA cluster, four-step column passes) with the selected butterfly.
 
     python tools/table1_b200.py [--batch 8192]
 
@@ -57,10 +59,15 @@ def main():
     out = {"paper_table1_cycles_per_bfly": {"Westmere": {"alg2": 10.1, "alg3": 6.9}, "SandyBridge": {"alg2": 9.1, "alg3": 5.9},
                                             "Piledriver": {"alg2": 13.9, "alg3": 12.0}},
            "shapes": {}}
-    for name, p, bits, ell, batch in (("paper L=2^11 62-bit p (p=1 mod 2^32)", P62, 64, 11, a.batch),
-                                      ("paper L=2^11 62-bit p (generic p)", P62G, 64, 11, a.batch),
-                                      ("C2 shape 4096 x 2^12 u64", P62, 64, 12, 4096),
-                                      ("u32 L=2^11, p=998244353", P30, 32, 11, a.batch)):
+    shapes = (("paper L=2^11 62-bit p (p=1 mod 2^32)", P62, 64, 11, a.batch),
+              ("paper L=2^11 62-bit p (generic p)", P62G, 64, 11, a.batch),
+              ("u32 L=2^11, p=998244353", P30, 32, 11, a.batch),
+              ("C1 1 x 2^10 u32 (latency)", P30, 32, 10, 1),
+              ("C2 4096 x 2^12 u64 (forward)", P62, 64, 12, 4096),
+              ("C3 1024 x 2^16 u32 p=998244353 (forward, 2-CTA cluster kernel)", P30, 32, 16, 1024),
+              ("C4 64 x 2^24 u64 (column pass with twiddle matrix + 2^15 cluster row pass)", P62, 64, 24, 64),
+              ("C5 1 x 2^28 u64 (two factored column passes + 2^12 row pass)", P62, 64, 28, 1))
+    for name, p, bits, ell, batch in shapes:
         r = {f"alg{alg}": run(p, bits, ell, batch, alg) for alg in (2, 3, 5)}
         r["alg2_over_alg3_time"] = r["alg2"]["ms"] / r["alg3"]["ms"]
         r["alg5_over_alg3_time"] = r["alg5"]["ms"] / r["alg3"]["ms"]
