@@ -151,6 +151,22 @@ ntt_status ntt_execute_host(ntt_plan_t plan, unsigned ops, const void* host_in, 
  * Returns NTT_ERR_UNSUPPORTED when ell > 20 (tables are factored then). */
 ntt_status ntt_plan_twiddles(ntt_plan_t plan, void* host_W, void* host_Wp);
 
+/* Copy a device-resident twiddle table the kernels read to host memory (test hook for A1, P:58,
+ * W' p <= W beta < (W'+1) p).  pass indexes ntt_plan_info_t.pass_log2.
+ *   kind 0: the per-stage table of that pass's sub-transform (length N = 2^pass_log2[pass], root
+ *           omega^(L/N)): stage i (1-based) at entry N - (N >> (i-1)) + (i-1), entries
+ *           zeta_i^k, k <= N >> i (the inverse reads the same table, negated entries).
+ *   kind 1, 2: the four-step twiddle factors of column pass `pass` (blocks of B = 2^(ell - sum of
+ *           the earlier passes) words, root omega_B): table A = omega_B^(e << H), e < B >> H, and
+ *           table B = omega_B^e, e < 2^H (H = log2 of B's entry count); a direct table has A = B.
+ *   kind 3: the twiddle matrix of column pass `pass`: N rows x S columns, entry (r, c) =
+ *           omega_B^(c rev(r)) (NTT_ERR_UNSUPPORTED when that level uses factors).
+ * Entries are (W, W') pairs of the plan's word size; Algorithm 5 plans' forward tables hold
+ * one word beta W mod p per entry.  *bytes receives the table size; host_out = NULL only
+ * queries it; otherwise capacity must be >= *bytes.  Synchronous. */
+ntt_status ntt_plan_table(ntt_plan_t plan, unsigned kind, unsigned pass, void* host_out, size_t capacity,
+                          size_t* bytes);
+
 /* ---- four-step pass entry points for a transform split over G GPUs (config C5) ----
  * View the length-L transform (L = 2^ell) as an N1 x N2 row-major matrix,
  * N1 = 2^ell1, N2 = L/N1, M[r][c] = x[N2 r + c].  Rank g of G holds the column

@@ -75,6 +75,7 @@ def _load() -> ctypes.CDLL:
         "ntt_execute_host": [vp, uint, vp, vp, sz, vp, sz, vp],
         "ntt_calibrate_butterfly": [uint, u64, u64, u64, uint, vp, ctypes.POINTER(u64), vp],
         "ntt_audit_counts": [c_int, ctypes.POINTER(u64)],
+        "ntt_plan_table": [vp, uint, uint, vp, sz, ctypes.POINTER(sz)],
         "ntt_audit_reset": [c_int, c_int],
     }
     for name, args in sig.items():
@@ -96,7 +97,7 @@ _lib = _load()
 
 EXPORTED = (
     "ntt_plan_create", "ntt_plan_create_ex", "ntt_plan_destroy", "ntt_plan_info", "ntt_forward", "ntt_inverse", "ntt_transform_pass", "ntt_pointwise_mul",
-    "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_fourstep_cols", "ntt_fourstep_rows",
+    "ntt_cyclic_convolve", "ntt_execute_host", "ntt_plan_twiddles", "ntt_plan_table", "ntt_fourstep_cols", "ntt_fourstep_rows",
     "ntt_fourstep_cols_inv", "ntt_fourstep_rows_inv", "ntt_fourstep_cols_p2p",
     "ntt_fourstep_rows_inv_p2p", "ntt_block_transpose", "ntt_crt3", "ntt_synth_uniform",
     "ntt_debug_butterfly", "ntt_calibrate_butterfly", "ntt_set_range_checks", "ntt_build_flags", "ntt_audit_counts", "ntt_audit_reset", "ntt_last_launch_count", "ntt_status_str", "ntt_last_cuda_error", "ntt_abi_version",
@@ -251,6 +252,18 @@ class Plan:
         Wp = np.zeros(max(half, 1), dtype=dt)
         _check(_lib.ntt_plan_twiddles(self._h, W.ctypes.data, Wp.ctypes.data), "ntt_plan_twiddles")
         return W[:half], Wp[:half]
+
+    def table(self, kind: int, pass_index: int = 0):
+        """ntt_plan_table: a device-resident twiddle table as a numpy array, shape (n, 2) of
+        (W, W') pairs (or (n,) one-word Montgomery entries for Algorithm 5 forward tables)."""
+        import numpy as np
+        nb = ctypes.c_size_t()
+        _check(_lib.ntt_plan_table(self._h, kind, pass_index, None, 0, ctypes.byref(nb)), "ntt_plan_table")
+        buf = np.empty(nb.value // self.word_bytes, dtype=np.uint64 if self.word_bytes == 8 else np.uint32)
+        _check(_lib.ntt_plan_table(self._h, kind, pass_index, buf.ctypes.data, nb.value, ctypes.byref(nb)),
+               "ntt_plan_table")
+        mont = self.butterfly == 5 and kind in (0, 1, 2, 3)
+        return buf.astype(np.uint64) if mont else buf.astype(np.uint64).reshape(-1, 2)
 
     def fourstep_cols(self, ell1, x_shard, rank, world, stream=None):
         _check(_lib.ntt_fourstep_cols(self._h, ell1, _ptr(x_shard), rank, world, _stream(stream)),

@@ -175,6 +175,7 @@ struct ntt_plan_s {
                            // Algorithm 5 plans (Montgomery tw_fwd) the Shoup table of omega
   std::vector<void*> sub_fwd, sub_inv;  // per pass sub-length tables (sub_inv[j] == sub_fwd[j])
   std::vector<void*> owned;
+  std::map<const void*, size_t> table_bytes;  // size of every uploaded table (ntt_plan_table)
   // lazily built tables for the distributed four-step entry points (guarded by mu)
   std::mutex mu;
   std::map<unsigned, void*> extra_sub;      // log2 N -> omega_N^e per-stage table (forward and inverse)
@@ -222,6 +223,7 @@ ntt_status upload(ntt_plan_s* pl, const std::vector<uint8_t>& host, void** out) 
   cudaError_t e = cudaMalloc(&d, n);
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? NTT_ERR_NOMEM : cuda_fail(e);
   pl->owned.push_back(d);
+  pl->table_bytes[d] = host.size();
   if (!host.empty()) {
     e = cudaMemcpy(d, host.data(), host.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -562,6 +564,42 @@ ntt_status ntt_plan_twiddles(ntt_plan_t pl, void* host_W, void* host_Wp) {
 }
 
 static bool aligned16(const void* x) { return ((uintptr_t)x & 15) == 0; }
+
+ntt_status ntt_plan_table(ntt_plan_t pl, unsigned kind, unsigned pass, void* host_out, size_t capacity,
+                          size_t* bytes) {
+  if (!pl || !bytes || kind > 3) return NTT_ERR_ARG;
+  *bytes = 0;
+  const unsigned np = (unsigned)pl->passes.size();
+  if (pass >= np || pl->ell == 0) return NTT_ERR_ARG;
+  const void* d = nullptr;
+  if (kind == 0) {
+    d = np == 1 ? pl->tw_fwd : pl->sub_fwd[pass];
+  } else {
+    if (pass + 1 >= np) return NTT_ERR_ARG;  // the row pass has no four-step twiddle
+    unsigned outer = 0;
+    for (unsigned i = 0; i < pass; ++i) outer += pl->passes[i];
+    const unsigned lb = pl->ell - outer;
+    if (kind == 3) {
+      void* fm = nullptr;
+      if (ntt_status st = fourstep_matrix(pl, lb, pl->passes[pass], &fm, pl->bfly); st != NTT_OK) return st;
+      d = fm;
+    } else {
+      ntt_plan_s::FsTables t{};
+      if (ntt_status st = fourstep_level_tables(pl, lb, &t, pl->bfly); st != NTT_OK) return st;
+      d = kind == 1 ? t.fa : t.fb;
+    }
+  }
+  if (!d) return NTT_ERR_UNSUPPORTED;  // e.g. no matrix at this level
+  std::lock_guard<std::mutex> lk(pl->mu);
+  auto it = pl->table_bytes.find(d);
+  if (it == pl->table_bytes.end()) return NTT_ERR_UNSUPPORTED;
+  *bytes = it->second;
+  if (!host_out) return NTT_OK;  // size query
+  if (capacity < it->second) return NTT_ERR_ARG;
+  DeviceGuard g(pl->device);
+  cudaError_t e = cudaMemcpy(host_out, d, it->second, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? NTT_OK : cuda_fail(e);
+}
 
 // On-chip transform of `batch` contiguous N-point transforms: the TMA-staged
 // kernel where it applies (NTT_DISABLE_TMA=1 forces the register-direct one).

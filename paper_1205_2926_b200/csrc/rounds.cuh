@@ -121,6 +121,11 @@ template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
 __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, const Mod<W>& m) {
   constexpr int S = 1 << SR;
   constexpr int D = (1 << LOGN) >> (LEVEL + SR);
+  // one base pointer per group, twi - c[q]: every entry m - k = (m - hh D) - c[q] of the round is then a
+  // compile-time offset from it (a per-load runtime index would cost an IMAD.WIDE address each)
+  const TwPair<W>* tq[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) tq[q] = twi - c[q];
 #pragma unroll
   for (int j = SR - 1; j >= 0; --j) {
     const int half = S >> (j + 1);
@@ -133,7 +138,7 @@ __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* _
         const bool unit = w1 || (D == 1 && hh == 0);  // k = 0: W = 1
         W w = 1, wp = 0;
         // negated twiddle -zeta^{-k} = zeta^{m - k} from the forward table (inv_index)
-        if (!unit) ldtw<W>(twi, (uint32_t)(off + ((1 << LOGN) >> (LEVEL + j + 1)) - (hh * D + c[q])), w, wp);
+        if (!unit) ldtw<W>(tq[q], (uint32_t)(off + ((1 << LOGN) >> (LEVEL + j + 1)) - hh * D), w, wp);
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;

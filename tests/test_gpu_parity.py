@@ -580,3 +580,84 @@ def test_transform_pass_sequence_equals_transform(ntt, p, bits, ell, batch):
     assert np.array_equal(to_host(a), to_host(b))
     with pytest.raises(ntt.NttError):
         plan.transform_pass(b, n)
+
+
+def _check_pairs(pairs, want_w, p, beta, idx):
+    """(W, W') pairs at sampled indices: W = want_w(i), W' p <= W beta < (W'+1) p."""
+    for i in idx:
+        We, Wpe = int(pairs[i, 0]), int(pairs[i, 1])
+        assert We == want_w(i), i
+        assert Wpe * p <= We * beta < (Wpe + 1) * p, i
+
+
+@pytest.mark.parametrize("p,bits,ell", [(P62, 64, 24), (P62, 64, 28), (P30, 32, 20), (P62, 64, 15)])
+def test_device_resident_tables(ntt, p, bits, ell):
+    """A1 on the tables the kernels actually read (ntt_plan_table): every pass's per-stage table
+    (stage i: zeta_i^k for k <= N >> i, the extra entry -1 included), the four-step factors and the
+    twiddle matrix of every column pass, checked entry by entry (sampled for the 2^20+ ones)."""
+    import random
+    L = 1 << ell
+    w = root(p, L)
+    beta = 1 << bits
+    plan = ntt.Plan(p, w, ell, bits)
+    info = plan.info()
+    sched = [info.pass_log2[i] for i in range(info.n_passes)]
+    rng = random.Random(ell)
+    outer = 0
+    for j, n in enumerate(sched):
+        N = 1 << n
+        rootN = pow(w, L // N, p)
+        t = plan.table(0, j)
+        assert t.shape[0] == N - 1 + n
+        for i in range(1, n + 1):
+            off = N - (N >> (i - 1)) + (i - 1)
+            zeta = pow(rootN, 1 << (i - 1), p)
+            m = N >> i
+            ks = range(m + 1) if m < 4096 else [0, 1, m - 1, m] + rng.sample(range(m), 500)
+            _check_pairs(t, lambda e, off=off, zeta=zeta: pow(zeta, e - off, p), p, beta, [off + k for k in ks])
+            assert int(t[off + m, 0]) == p - 1  # zeta_i^{m_i} = -1: the inverse's negated entries rely on it
+        if j + 1 < len(sched):
+            lb = ell - outer
+            B = 1 << lb
+            wB = pow(w, L >> lb, p)
+            fa, fb = plan.table(1, j), plan.table(2, j)
+            H = int(fb.shape[0]).bit_length() - 1
+            if fa.shape[0] == B and fb.shape[0] == B:
+                H = 0  # direct table
+            if H:
+                _check_pairs(fb, lambda e: pow(wB, e, p), p, beta, range(fb.shape[0]))
+                _check_pairs(fa, lambda e: pow(wB, e << H, p), p, beta,
+                             rng.sample(range(fa.shape[0]), min(2000, fa.shape[0])))
+            else:
+                _check_pairs(fa, lambda e: pow(wB, e, p), p, beta, rng.sample(range(B), min(4000, B)))
+            try:
+                M = plan.table(3, j)
+            except ntt.NttError:
+                M = None
+            if M is not None:
+                S = B >> n
+                assert M.shape[0] == N * S
+                idx = rng.sample(range(N * S), 3000) + [0, S - 1, (N - 1) * S, N * S - 1]
+                _check_pairs(M, lambda e: pow(wB, (e % S) * bitrev(e // S, n), p), p, beta, idx)
+            outer += n
+
+
+def test_device_resident_tables_alg5(ntt):
+    """F2 tables hold one word W'_mont = beta W mod p per entry: per-stage, factors, matrix."""
+    import random
+    p, bits, ell = P62, 64, 24
+    L = 1 << ell
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits, butterfly=5)
+    beta = 1 << bits
+    n0, n1 = plan.info().pass_log2[0], plan.info().pass_log2[1]
+    t = plan.table(0, 1)  # the row pass's per-stage table (one word per entry)
+    N = 1 << n1
+    rootN = pow(w, L // N, p)
+    assert t.shape[0] == N - 1 + n1
+    for k in range(0, N // 2 + 1, 97):
+        assert int(t[k]) == pow(rootN, k, p) * beta % p
+    M = plan.table(3, 0)
+    S = L >> n0
+    for e in random.Random(3).sample(range(M.shape[0]), 2000):
+        assert int(M[e]) == pow(w, (e % S) * bitrev(e // S, n0), p) * beta % p

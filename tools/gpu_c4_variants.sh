@@ -1,7 +1,7 @@
 # C4 A/B: the forward twiddle matrix and the column-pass tile order
 O=gpurun_out/${OUT:-c4var}
 mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS:-} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 tail -3 $O/pytest_gpu.log
 run() { # name env...
   local name=$1; shift
