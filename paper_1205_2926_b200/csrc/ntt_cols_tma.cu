@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "fourstep.cuh"
 #include "internal.h"
@@ -175,14 +176,23 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     fence_mbar_init();
   }
   __syncthreads();
-  uint64_t tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < prm.n_tiles) cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, tile, prm, buf_of(0), bar_of(0));
+  // tiles: grid-stride, or (twiddle-matrix passes with bmajor == 2) one contiguous range per CTA, so a
+  // CTA walks one column group through every block before the next and its matrix rows stay on chip
+  uint64_t tile = blockIdx.x, tend = prm.n_tiles, tstep = gridDim.x;
+  if constexpr (TWM == 2) {
+    if (prm.bmajor == 2) {
+      tile = prm.n_tiles * blockIdx.x / gridDim.x;
+      tend = prm.n_tiles * (blockIdx.x + 1) / gridDim.x;
+      tstep = 1;
+    }
+  }
+  if (threadIdx.x == 0 && tile < tend) cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, tile, prm, buf_of(0), bar_of(0));
   W v[Sh::E];
-  for (uint32_t it = 0; tile < prm.n_tiles; ++it, tile += gridDim.x) {
+  for (uint32_t it = 0; tile < tend; ++it, tile += tstep) {
     const int cur = it & 1;
-    const uint64_t next = tile + gridDim.x;
+    const uint64_t next = tile + tstep;
     if constexpr (Sh::R == 1) {  // no exchange to hide the prefetch behind: issue it now
-      if (threadIdx.x == 0 && next < prm.n_tiles) {
+      if (threadIdx.x == 0 && next < tend) {
         bulk_wait_read0();
         cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, next, prm, buf_of(cur ^ 1), bar_of(cur ^ 1));
       }
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
     constexpr int r0 = INV ? Sh::R - 1 : 0;
     cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, fm, m, &tmap, next,
-                                                    buf_of(cur ^ 1), bar_of(cur ^ 1), Sh::R > 1 && next < prm.n_tiles);
+                                                    buf_of(cur ^ 1), bar_of(cur ^ 1), Sh::R > 1 && next < tend);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();
     if constexpr (P2P) {
@@ -241,6 +251,17 @@ template <class W, int LOGN> struct ColsTmaLE {
       sizeof(W) == 8 ? (LOGN == 9 ? NTT_COLS_LE64_9 : (LOGN < 4 ? LOGN : 4)) : (LOGN < 5 ? LOGN : 5);
 };
 
+// L2 promotion of the tile loads (A/B hook NTT_COLS_L2PROMO = 0 / 128 / 256, default 256: a tile's
+// 128-byte row segments pull their neighbour column group's half of each 256-byte line into L2)
+static CUtensorMapL2promotion cols_l2_promotion() {
+  static const int v = [] {
+    const char* e = getenv("NTT_COLS_L2PROMO");
+    return e ? atoi(e) : 256;
+  }();
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : (v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+}
+
 template <class W, int LOGN, bool INV, bool PLO1, bool P2P, int TWM, int BF = 3>
 static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTables& tb, uint64_t p, cudaStream_t s) {
   constexpr int LE = ColsTmaLE<W, LOGN>::value;
@@ -255,7 +276,7 @@ static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTable
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, x, dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    cols_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, TWM, BF>;
   static PerDevice occ_cache;
