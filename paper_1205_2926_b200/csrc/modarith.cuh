@@ -80,14 +80,26 @@ __device__ __forceinline__ uint64_t mulhi_chain(uint64_t a, uint64_t b) {
   return r;
 }
 
-// Conditional subtraction x >= m ? x - m : x for x < 2m, m <= beta/2 (every use: m in
-// {p, 2p}, p < beta/4).  Then x - m lies in (-beta/2, beta/2), so its sign decides:
-// u64 selects on the sign word (no 64-bit compare pair); u32 uses min(x, x - m).
-// Measured +4% on the register-only u64 butterfly (tools/bfly_variants.cu).
+// Conditional subtraction x >= m ? x - m : x (every use: x < 2m, m in {p, 2p}, p < beta/4).
+// u64 selects on the carry of x + (2^64 - m) (round 2; the sign test of x - m with NTT_CSUB_SIGN,
+// round 1's form); u32 uses min(x, x - m) (one VIADDMNMX).
 template <class W> __device__ __forceinline__ W csub(W x, W m);
 template <> __device__ __forceinline__ uint64_t csub<uint64_t>(uint64_t x, uint64_t m) {
+#ifndef NTT_CSUB_SIGN
+  // x + (2^64 - m) carries out exactly when x >= m: the carry of the high word's add is the select
+  // predicate (IADD3, IADD3.X with carry-out, 2 SEL), one instruction fewer than the sign test of
+  // x - m (tools/bfly_hi64.cu); 2^64 - m is loop-invariant and hoisted
+  uint64_t r;
+  asm("{\n\t.reg .u32 x0,x1,n0,n1,d0,d1,c;\n\t.reg .pred q;\n\t"
+      "mov.b64 {x0,x1}, %1;\n\tmov.b64 {n0,n1}, %2;\n\t"
+      "add.cc.u32 d0, x0, n0;\n\taddc.cc.u32 d1, x1, n1;\n\taddc.u32 c, 0, 0;\n\t"
+      "setp.ne.u32 q, c, 0;\n\tselp.u32 d0, d0, x0, q;\n\tselp.u32 d1, d1, x1, q;\n\t"
+      "mov.b64 %0, {d0,d1};\n\t}" : "=l"(r) : "l"(x), "l"(0 - m));
+  return r;
+#else
   const int64_t d = (int64_t)(x - m);
   return d < 0 ? x : (uint64_t)d;
+#endif
 }
 template <> __device__ __forceinline__ uint32_t csub<uint32_t>(uint32_t x, uint32_t m) { return umin(x, x - m); }
 

@@ -44,16 +44,31 @@ __device__ __forceinline__ uint64_t hi64_v3(uint64_t a, uint64_t b) {
   return r;
 }
 template <int V> __device__ __forceinline__ uint64_t hi64(uint64_t a, uint64_t b) {
-  if constexpr (V == 0) return __umul64hi(a, b);
+  if constexpr (V == 0 || V == 4) return __umul64hi(a, b);
+  else if constexpr (V == 5) return hi64_v3(a, b);
   else if constexpr (V == 1) return hi64_v1(a, b);
   else if constexpr (V == 2) return hi64_v2(a, b);
   else return hi64_v3(a, b);
 }
+// conditional subtraction by the carry of x + (2^64 - m): x >= m exactly when that add carries out
+__device__ __forceinline__ uint64_t csub_cc(uint64_t x, uint64_t nm) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 x0,x1,n0,n1,d0,d1,c;\n\t.reg .pred q;\n\t"
+      "mov.b64 {x0,x1}, %1;\n\tmov.b64 {n0,n1}, %2;\n\t"
+      "add.cc.u32 d0, x0, n0;\n\taddc.cc.u32 d1, x1, n1;\n\taddc.u32 c, 0, 0;\n\t"
+      "setp.ne.u32 q, c, 0;\n\tselp.u32 d0, d0, x0, q;\n\tselp.u32 d1, d1, x1, q;\n\t"
+      "mov.b64 %0, {d0,d1};\n\t}" : "=l"(r) : "l"(x), "l"(nm));
+  return r;
+}
 template <int V>
 __device__ __forceinline__ void bf(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t wp, uint64_t p2, uint32_t np1) {
   uint64_t s = X + Y;
-  const int64_t d = (int64_t)(s - p2);
-  s = d < 0 ? s : (uint64_t)d;
+  if constexpr (V >= 4) {
+    s = csub_cc(s, 0 - p2);
+  } else {
+    const int64_t d = (int64_t)(s - p2);
+    s = d < 0 ? s : (uint64_t)d;
+  }
   const uint64_t T = X - Y + p2;
   const uint64_t Q = hi64<V>(wp, T);
   Y = tail_plo1(Q, w * T, np1);
@@ -121,6 +136,8 @@ int main() {
     bench(k<1, 256>, 256, bps, "V1 mul.hi + 3 mul.wide + add.cc");
     bench(k<2, 256>, 256, bps, "V2 64-bit accumulate");
     bench(k<3, 256>, 256, bps, "V3 mad.lo.cc/madc.hi chain");
+    bench(k<4, 256>, 256, bps, "V4 library hi64 + carry csub");
+    bench(k<5, 256>, 256, bps, "V5 chain hi64 + carry csub");
   }
   return 0;
 }
