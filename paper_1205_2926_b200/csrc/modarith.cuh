@@ -61,8 +61,9 @@ template <> struct alignas(16) TwPair<uint64_t> { uint64_t w, wp; };
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
 // hi64(a b) as a 32-bit multiply-add carry chain (mad.lo.cc / madc.hi): fewer IMAD.X carry fix-ups
-// than __umul64hi's expansion; measured 4% faster in the inverse (Algorithm 4) kernels, neutral
-// in the forward ones, so shoup_mul takes it only where requested (CHAIN).
+// than __umul64hi's expansion; measured 4% faster in the inverse (Algorithm 4) kernels, and with the
+// carry-select csub 2-4% in the register-only forward loop (tools/bfly_hi64.cu), so it is shoup_mul's
+// default (NTT_SHOUP_CHAIN_DEFAULT=false restores __umul64hi for A/B builds).
 __device__ __forceinline__ uint64_t mulhi_chain(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("{\n\t.reg .u32 a0,a1,b0,b1,t,m1,h0,h1;\n\t"
@@ -126,7 +127,10 @@ template <class W> __device__ __forceinline__ Mod<W> make_mod(W p) {
 // returns WT - Qp in [0, 2p), congruent to W*T mod p, Q = floor(W'T/beta).
 // PLO1 (beta = 2^64, p = 1 mod 2^32): Qp mod beta = Q + (q0 * p_hi) << 32, so the
 // low product costs one 32-bit IMAD instead of a 64 x 64 -> 64 multiply.
-template <class W, bool PLO1 = false, bool CHAIN = false>
+#ifndef NTT_SHOUP_CHAIN_DEFAULT
+#define NTT_SHOUP_CHAIN_DEFAULT true
+#endif
+template <class W, bool PLO1 = false, bool CHAIN = NTT_SHOUP_CHAIN_DEFAULT>
 __device__ __forceinline__ W shoup_mul(W T, W w, W wp, const Mod<W>& m) {
   W Q;
   if constexpr (sizeof(W) == 8 && CHAIN) Q = mulhi_chain(wp, T);

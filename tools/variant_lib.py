@@ -1,7 +1,7 @@
 """Build an experimental copy of libntt_b200.so with extra nvcc flags (e.g. -DNTT_TMA_LE64=3),
 recompiling only the listed sources and linking them with the default objects.
-    python tools/variant_lib.py NAME "FLAGS" [src.cu ...]  -> variants/libntt_NAME.so
-Load it with NTT_B200_LIB=variants/libntt_NAME.so (tools/time_cfg.py)."""
+    python tools/variant_lib.py NAME "FLAGS" [src.cu ...]  -> abvar/libntt_NAME.so (gitignored; travels to the GPU box)
+Load it with NTT_B200_LIB=abvar/libntt_NAME.so (tools/time_cfg.py)."""
 import os
 import shlex
 import subprocess
@@ -16,7 +16,7 @@ def main():
     name, flags = sys.argv[1], shlex.split(sys.argv[2])
     srcs = sys.argv[3:] or ["ntt_contig_tma.cu"]
     _build.build()
-    out = os.path.join(ROOT, "variants")
+    out = os.path.join(ROOT, os.environ.get("NTT_VARIANT_DIR", "abvar"))
     os.makedirs(os.path.join(out, name), exist_ok=True)
     objs = []
     for s in _build.SOURCES:
