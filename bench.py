@@ -464,11 +464,15 @@ def run_native(args, cfg, rank, world, local_rank):
     st_mul = sum(wk[k][0] * n for k, n in per_step.items()) / alu_peak * 1e3
     st_hbm = sum(wk[k][1] * n for k, n in per_step.items()) / (hbm_peak * 1e9) * 1e3
     step_mean = total_ms / args.steps
+    # DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
+    # (profiles/ncu_traffic.json: config -> "per_pass" -> pass name -> dram_bytes_per_launch)
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         entry = prof.get(args.config, {})
-        traffic = entry.get(dom, entry).get("dram_bytes_per_launch") if isinstance(entry.get(dom, entry), dict) else None
+        traffic = entry.get("per_pass", {}).get(dom, {}).get("dram_bytes_per_launch")
+        if traffic is None and not entry.get("per_pass"):
+            traffic = entry.get("dram_bytes_per_launch")
     except Exception:
         pass
     roofline = {

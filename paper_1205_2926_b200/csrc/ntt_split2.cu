@@ -140,9 +140,9 @@ struct SplitStage {
   const CUtensorMap* map_a;  // forward with PW: 128-byte rows of a (a-hat in, c-hat out)
 };
 
-#ifndef NTT_SPLIT_NX
-#define NTT_SPLIT_NX 3
-#endif
+#ifndef NTT_SPLIT_NX  // spare staging slots of the K = 2 forward (A/B on one box, round 2: 2 slots
+#define NTT_SPLIT_NX 2    // beat 3 -- C4 row pass 10.68 -> 10.61 ms, C3 2.537 -> 2.523 ms -- the smaller
+#endif                    // shared-memory footprint leaves more L1 to the twiddle loads)
 
 // Forward staging (K = 2): the first round's inputs x_{hD + t} and x_{Q + hD + t} (h < 32) come in
 // NCH chunks of HC h-rows of both blocks (2 x HC x D words; one TMA box of 128-byte rows per
