@@ -661,3 +661,43 @@ def test_device_resident_tables_alg5(ntt):
     S = L >> n0
     for e in random.Random(3).sample(range(M.shape[0]), 2000):
         assert int(M[e]) == pow(w, (e % S) * bitrev(e // S, n0), p) * beta % p
+
+
+def test_execute_host_threads_share_a_plan(ntt):
+    """ntt_execute_host from several host threads on one plan (the header's thread-safety contract):
+    each call enqueues its whole pipeline under the plan's lock, on its own stream and device buffer,
+    and every result equals the device-resident transform."""
+    import threading
+    p, bits, ell, batch = P62, 64, 12, 300
+    L = 1 << ell
+    plan = ntt.Plan(p, root(p, L), ell, bits)
+    nthr = 4
+    xs, refs, outs, errs = [], [], [], []
+    for i in range(nthr):
+        x = torch.empty(batch * L, dtype=torch.uint64, device="cuda")
+        ntt.synth_uniform(x, synth.config_seed(2), 40 + i, bound=p)
+        r = x.clone()
+        plan.forward(r)
+        xs.append(x.cpu().pin_memory())
+        refs.append(r.cpu())
+        outs.append(torch.empty_like(xs[-1]).pin_memory())
+    torch.cuda.synchronize()
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            dbuf = torch.empty(16 * L, dtype=torch.uint64, device="cuda")
+            for _ in range(3):
+                plan.execute_host(ntt.NTT_OP_FORWARD, xs[i], outs[i], dbuf, stream=s)
+            s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(nthr)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(nthr):
+        assert torch.equal(outs[i].view(torch.int64), refs[i].view(torch.int64)), i
