@@ -534,7 +534,10 @@ def run_native(args, cfg, rank, world, local_rank):
         h_in = torch.empty(batch * L, dtype=dt, pin_memory=True)
         h_in.copy_(x0.cpu())
         h_out = torch.empty_like(h_in).pin_memory()
-        dbuf = torch.empty(max(L, min(batch * L, (64 << 20) // wb)), dtype=dt, device=dev)
+        # device scratch of the host pipeline: room for its 4-slot ring (>= 4 transforms, or >= 64 MiB), so
+        # the H2D copy of one chunk, the transform of the next and the D2H of a third overlap
+        dbuf_words = min(batch * L, max(4 * L, (64 << 20) // wb))
+        dbuf = torch.empty(dbuf_words, dtype=dt, device=dev)
         for _ in range(2):
             plans[0].execute_host(ops, h_in, h_out, dbuf, stream=stream)
         stream.synchronize()
