@@ -61,7 +61,8 @@ struct ColsParams {
   uint32_t log_tw_mul;     // log2(L / B): converts block-root exponents to omega_L exponents
   uint32_t ell;            // log2 L
   uint32_t H;              // factored-table split (0 = direct table of L entries)
-  uint32_t twiddle;        // 0: no four-step twiddle; 1: apply it
+  uint32_t twiddle;        // 1: apply the four-step twiddle (always 1: k_cols_tma's forward applies it
+                           // unconditionally, its last stage's W = 1 butterflies being left lazy for it)
   uint32_t normalize;      // 1: write canonical [0,p) output
   // distributed shard (config C5): global column = col_map(local column)
   uint32_t shard;          // 0: plain; 1: local columns map to global via the fields below

@@ -190,6 +190,20 @@ template <class W> __device__ __forceinline__ void bfly_alg3_w1(W& X, W& Y, W p2
   NTT_AUDIT(Y, p2);
 }
 
+// The W = 1 butterfly without its two corrections, outputs in [0,4p): X + Y and X - Y + 2p (congruent
+// to X + Y and X - Y).  Only where a Shoup / Montgomery product follows on every output (dif_round
+// LAZY_LAST), which accepts any T < beta and returns [0,2p).
+template <class W> __device__ __forceinline__ void bfly_alg3_w1_lazy(W& X, W& Y, W p2) {
+  NTT_AUDIT(X, p2);
+  NTT_AUDIT(Y, p2);
+  const W s = X + Y;
+  W T = X - Y + p2;
+  if (NTT_AUDIT_MUTATED()) T = X - Y;
+  NTT_AUDIT(T, 2 * p2);
+  X = s;
+  Y = T;
+}
+
 // Algorithm 4, the modified inverse butterfly:
 // X, Y in [0,4p) -> X' = X + WY, Y' = X - WY, both in [0,4p)  (Theorem 3).
 template <class W, bool PLO1 = false>

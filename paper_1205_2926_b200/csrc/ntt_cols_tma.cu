@@ -93,7 +93,9 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
         }
     }
   }
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF>(v, c, tw, m);
+  // forward column passes multiply every output by the four-step twiddle next: the last stage's W = 1
+  // butterflies skip their corrections (LAZY_LAST); prm.twiddle is 1 for every forward column pass
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF, last>(v, c, tw, m);
   else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (!last) {
     __syncthreads();
@@ -103,8 +105,8 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
     }
   }
   if constexpr (last) {
-    if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT
-      if (prm.twiddle) {
+    if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT (every forward
+      {                    // column pass has one; the lazy last stage above relies on it)
 #pragma unroll
         for (int q = 0; q < G; ++q)
 #pragma unroll

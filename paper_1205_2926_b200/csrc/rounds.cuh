@@ -87,7 +87,11 @@ template <int LOGN, int LE, int ra, int rb> __host__ __device__ constexpr bool w
 // BF selects the butterfly: 3 = Algorithm 3 (the product path), 2 = Algorithm 2 and
 // 5 = Algorithm 5 (ablations F1/F2 of SURVEY.md §8(f); Alg. 5 reads W' = beta W mod p
 // from a one-word-per-entry table, ldtw_bf).
-template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3>
+// LAZY_LAST: the transform's last stage (m = 1, W = 1) leaves X + Y and X - Y + 2p unreduced, in [0,4p):
+// only for callers that multiply every output by a twiddle next (the four-step column pass), since a
+// Shoup product takes any T < beta and returns [0,2p) -- the two corrections of P:226's W = 1
+// butterfly are then redundant.
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3, bool LAZY_LAST = false>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
   constexpr int S = 1 << SR;
   constexpr int D = (1 << LOGN) >> (LEVEL + SR);
@@ -107,7 +111,8 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
 #pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (unit) bfly_fwd_w1<W, BF>(v[q * S + h], v[q * S + h + half], m);
+          if (LAZY_LAST && BF != 2 && w1) bfly_alg3_w1_lazy<W>(v[q * S + h], v[q * S + h + half], m.p2);
+          else if (unit) bfly_fwd_w1<W, BF>(v[q * S + h], v[q * S + h + half], m);
           else bfly_fwd<W, PLO1, BF>(v[q * S + h], v[q * S + h + half], w, wp, m);
         }
       }
