@@ -369,6 +369,8 @@ template <class W> __device__ __forceinline__ W norm4(W x, W p, W p2) {
 // for a, b < 2p: ab < 4p^2 < p beta, so R1 < p and the result lies in (0, 2p),
 // congruent to a b beta^{-1} mod p.
 template <class W> __device__ __forceinline__ W mont_redc_mul(W a, W b, W J, W p) {
+  NTT_AUDIT(a, 2 * p);  // the REDC's precondition ab < 4p^2 < p beta
+  NTT_AUDIT(b, 2 * p);
   W R1, R0;
   mul_wide(a, b, R1, R0);
   W Q = R0 * J;
