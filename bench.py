@@ -706,6 +706,10 @@ def main():
     # the reference arm (CPU oracle) runs on rank 0 alone, also when --gpus N is given without torchrun
     world = int(env_world) if env_world is not None else args.gpus
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # plumbing test hook (not for measurements): every rank on GPU 0 over gloo, so the N > 1 code path
+    # (sharding, max-over-ranks timing, the JSON line) can be exercised on a one-GPU box
+    if os.environ.get("NTT_BENCH_PLUMBING_1GPU") == "1":
+        local_rank = 0
     nthreads = len(os.sched_getaffinity(0))
 
     if args.impl == "reference":
@@ -730,7 +734,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("NTT_BENCH_PLUMBING_1GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_native(args, cfg, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
