@@ -72,10 +72,12 @@ ntt_status ntt_plan_destroy(ntt_plan_t plan);
 /* Same, with the forward butterfly selectable for the paper's own comparison (Table 1,
  * P:212-228): NTT_BFLY_ALG3 = Algorithm 3 (default, the hot
  * path), NTT_BFLY_ALG2 = Algorithm 2 (NTL, canonical operands; forward input must be
- * < p), NTT_BFLY_ALG5 = Algorithm 5 (Montgomery; table holds W' = beta W mod p).
- * ALG2/ALG5 plans support ntt_forward only for on-chip lengths 2^8..2^13 (beta=2^64) /
- * 2^8..2^14 (beta=2^32); other calls return NTT_ERR_UNSUPPORTED.  ntt_inverse always
- * uses Algorithm 4. */
+ * < p), NTT_BFLY_ALG5 = Algorithm 5 (Montgomery; its forward tables hold one word
+ * W' = beta W mod p per entry, half the bytes of the Shoup pairs).  ALG2/ALG5 forward
+ * transforms run in every forward kernel family: lengths 2^8..2^28 for beta = 2^64 (on-chip,
+ * 2-CTA cluster and four-step column passes incl. the twiddle matrix) and 2^8..2^16 for
+ * beta = 2^32; other lengths return NTT_ERR_UNSUPPORTED.  ntt_inverse always uses
+ * Algorithm 4 (with the Shoup tables). */
 #define NTT_BFLY_ALG2 2u
 #define NTT_BFLY_ALG3 3u
 #define NTT_BFLY_ALG5 5u
