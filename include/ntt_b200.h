@@ -285,9 +285,11 @@ unsigned ntt_set_range_checks(unsigned on);
  *   ntt_build_flags: NTT_BUILD_RANGE_AUDIT when this library is the audit build.
  *   ntt_audit_counts: synchronises `device` and returns the violations counted since the last
  *     reset.  NTT_ERR_UNSUPPORTED in the production build.
- *   ntt_audit_reset: synchronises, zeroes the counters; mutate != 0 drops the "+2p" of Algorithm 3
- *     line 3 in every kernel (the mutation control), which the audit must report.
- *     NTT_ERR_UNSUPPORTED in the production build. */
+ *   ntt_audit_reset: synchronises, zeroes the counters; mutate bit 0 drops the "+2p" of Algorithm 3
+ *     line 3 in every kernel (the mutation control), which the audit must report; bit 1
+ *     turns on race stress: every round of every kernel starts with a per-warp pseudo-random delay,
+ *     so a missing barrier around a shared-memory exchange or a staging buffer would show up as wrong
+ *     results.  NTT_ERR_UNSUPPORTED in the production build. */
 #define NTT_BUILD_RANGE_AUDIT 1u
 unsigned ntt_build_flags(void);
 ntt_status ntt_audit_counts(int device, uint64_t* violations);

@@ -160,9 +160,10 @@ def audit_counts(device: int = 0) -> int:
     return int(v.value)
 
 
-def audit_reset(device: int = 0, mutate: bool = False):
-    """ntt_audit_reset: zero the counters; mutate drops Algorithm 3's "+2p" (audit build only)."""
-    _check(_lib.ntt_audit_reset(device, 1 if mutate else 0), "ntt_audit_reset")
+def audit_reset(device: int = 0, mutate: bool = False, stress: bool = False):
+    """ntt_audit_reset: zero the counters; mutate drops Algorithm 3's "+2p"; stress adds per-warp random
+    delays at every round (audit build only)."""
+    _check(_lib.ntt_audit_reset(device, (1 if mutate else 0) | (2 if stress else 0)), "ntt_audit_reset")
 
 
 def last_launch_count() -> int:

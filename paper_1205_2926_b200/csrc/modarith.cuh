@@ -46,12 +46,27 @@ __device__ __forceinline__ void audit_lt(uint64_t x, uint64_t bound) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.u64 p, %0, %1;\n\t@p red.global.add.u64 [%2], 1;\n\t}"
                :: "l"(x), "l"(bound), "l"(&d_audit_count) : "memory");
 }
-__device__ __forceinline__ bool audit_mutated() { return *(volatile int*)&d_audit_mutate != 0; }
+// d_audit_mutate bit 0: the mutation control; bit 1: race stress -- every round starts (before it reads its
+// inputs, and again before its butterflies) with a per-warp pseudo-random delay (up to ~4 us), so warps drift apart and a missing barrier between the rounds' shared-
+// memory exchanges (or a TMA buffer reused too early) would surface as wrong results (compute-sanitizer's
+// racecheck is not available on the pool)
+__device__ __forceinline__ bool audit_mutated() { return (*(volatile int*)&d_audit_mutate & 1) != 0; }
+__device__ __forceinline__ void audit_stress_point() {
+  if (*(volatile int*)&d_audit_mutate & 2) {
+    uint32_t h = (uint32_t)clock64() ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    __nanosleep(h & 4095u);
+  }
+}
 #define NTT_AUDIT(x, b) ::nttb::audit_lt((uint64_t)(x), (uint64_t)(b))
 #define NTT_AUDIT_MUTATED() ::nttb::audit_mutated()
+#define NTT_AUDIT_STRESS() ::nttb::audit_stress_point()
 #else
 #define NTT_AUDIT(x, b) ((void)0)
 #define NTT_AUDIT_MUTATED() false
+#define NTT_AUDIT_STRESS() ((void)0)
 #endif
 
 template <class W> struct TwPair;               // (W, W') twiddle pair, stored adjacently

@@ -30,6 +30,7 @@ __device__ __forceinline__ void cols_round(W* v, W* __restrict__ xb, W* sm, int 
                                            const ColsParams& prm, const TwPair<W>* __restrict__ tw,
                                            const TwPair<W>* __restrict__ fa, const TwPair<W>* __restrict__ fb,
                                            const Mod<W>& m) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay before the round reads its inputs
   const W p = m.p, p2 = m.p2;
   using Sh = ColsShape<W, LOGN, LE>;
   using RC = typename Sh::RC;

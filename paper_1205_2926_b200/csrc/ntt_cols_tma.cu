@@ -57,6 +57,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
                                                const Mod<W>& m, const CUtensorMap* map, uint64_t next_tile,
                                                uint32_t next_buf,
                                                uint32_t next_bar, bool prefetch) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay before the round reads its inputs
   using Sh = ColsTmaShape<W, LOGN, LE>;
   using RC = typename Sh::RC;
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);

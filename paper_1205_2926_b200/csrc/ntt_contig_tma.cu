@@ -53,6 +53,7 @@ __device__ __forceinline__ void tma_round(W* v, W* __restrict__ xb, W* sb, int t
                                           const TwPair<W>* __restrict__ tw, const Mod<W>& m, bool norm,
                                           bool first_exchange, const CUtensorMap* map, size_t next_tile,
                                           size_t ntiles, uint32_t next_buf, uint32_t next_bar) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay before the round reads its inputs
   using Sh = TmaShape<W, LOGN, LE>;
   using RC = typename Sh::RC;
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);

@@ -57,6 +57,7 @@ template <class W, int LOGN, int LE, bool INV, bool GATHER, bool PLO1, int r>
 __device__ __forceinline__ void contig_round(W* v, W* __restrict__ xb, const W* __restrict__ gin, size_t row,
                                              const GatherArgs& ga, W* sb, int t, bool active,
                                              const TwPair<W>* __restrict__ tw, const Mod<W>& m, bool norm) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay before the round reads its inputs
   const W p = m.p, p2 = m.p2;
   using Sh = ContigShape<LOGN, LE>;
   using RC = typename Sh::RC;

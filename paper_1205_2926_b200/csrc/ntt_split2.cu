@@ -185,6 +185,7 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
   const uint32_t sbase = smem_u32(sm);
   const int tsw = tswz<W>(t);  // (h - h0) D is a multiple of the swizzle period
   const int off = stage_off(LOGL, 1);
+  NTT_AUDIT_STRESS();
 #pragma unroll
   for (int k = 0; k < F::NCH; ++k) {
     mbar_wait(sbase + F::BAR_OFF + 8 * k, st.phase);
@@ -232,6 +233,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
                                             const TwPair<W>* __restrict__ tw_full, const Mod<W>& m,
                                             const PwArgs& pw, size_t boff, cg::cluster_group& cluster,
                                             const SplitStage& st) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay before the round reads its inputs
   using Sh = SplitShape<LOGQ, LE, K, (int)sizeof(W)>;
   using RC = typename Sh::RC;
   constexpr int Q = Sh::Q, SS = Sh::S_SPLIT, LOGL = Sh::LOGL;

@@ -885,7 +885,7 @@ ntt_status ntt_audit_reset(int device, int mutate) {
   if (e != cudaSuccess) return cuda_fail(e);
   for (const auto& tu : audit_tus()) {
     tu.reset();
-    tu.mutate(mutate ? 1 : 0);
+    tu.mutate(mutate & 3);  // bit 0: mutation control, bit 1: race stress
   }
   return NTT_OK;
 #else

@@ -93,6 +93,7 @@ template <int LOGN, int LE, int ra, int rb> __host__ __device__ constexpr bool w
 // butterfly are then redundant.
 template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3, bool LAZY_LAST = false>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
+  NTT_AUDIT_STRESS();  // audit build only: per-warp random delay (race stress)
   constexpr int S = 1 << SR;
   constexpr int D = (1 << LOGN) >> (LEVEL + SR);
 #pragma unroll
@@ -124,6 +125,7 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
 // zeta_i^{-k}, read as their negations from the forward table (inv_index, bfly_alg4n).
 template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
 __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, const Mod<W>& m) {
+  NTT_AUDIT_STRESS();
   constexpr int S = 1 << SR;
   constexpr int D = (1 << LOGN) >> (LEVEL + SR);
   // one base pointer per group, twi - c[q]: every entry m - k = (m - hh D) - c[q] of the round is then a

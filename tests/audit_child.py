@@ -65,6 +65,38 @@ def conv(batch):
     return fn
 
 
+def stress_case(name, p, bits, ell, batch, ops=("fwd", "inv"), conv=False):
+    """The same transform with and without race stress (per-warp random delays at every round): the
+    results must be identical and the range audit clean."""
+    L = 1 << ell
+    plan = ntt.Plan(p, root(p, L), ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(batch * L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(8), ell, bound=p)
+    outs, ms = [], []
+    for stress in (False, False, True):  # the first run loads the kernels (lazy module loading): untimed
+        ntt.audit_reset(0, stress=stress)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if conv:
+            a = x.clone().view(batch, L)
+            b = x.clone().view(batch, L).flip(0).contiguous()
+            plan.cyclic_convolve(a, b)
+            y = a.view(-1)
+        else:
+            y = x.clone()
+            for op in ops:
+                (plan.forward if op == "fwd" else plan.inverse)(y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        outs.append((y.view(torch.int64) if bits == 64 else y.view(torch.int32)).clone())
+        viol = ntt.audit_counts(0)
+    ntt.audit_reset(0)
+    out["STRESS " + name] = {"identical": bool(torch.equal(outs[1], outs[2]) and torch.equal(outs[0], outs[2])),
+                             "violations": viol, "ms_plain": round(ms[1], 3), "ms_stressed": round(ms[2], 3)}
+
+
 assert ntt.audit_build(), "NTT_B200_LIB=audit did not load the audit build"
 out = {}
 which = sys.argv[1:] or ["all"]
@@ -82,4 +114,12 @@ if "all" in which or "mutant" in which:
     case("MUTANT C2 4096 x 2^12 u64 fwd", transform(P62, 64, 12, 4096, ops=("fwd",)), mutate=True)
     case("MUTANT C4 shape 1 x 2^24 u64 fwd", transform(P62, 64, 24, 1, ops=("fwd",)), mutate=True)
     case("MUTANT 2^16 u32 fwd", transform(P30, 32, 16, 8, ops=("fwd",)), mutate=True)
+if "all" in which or "stress" in which:
+    stress_case("C2 4096 x 2^12 u64 fwd+inv", P62, 64, 12, 4096)
+    stress_case("2^15 u64 cluster fwd+inv", P62, 64, 15, 64)
+    stress_case("2^16 u32 cluster fwd+inv", P30, 32, 16, 64)
+    stress_case("2^16 u32 convolution (fused pointwise)", P30, 32, 16, 32, conv=True)
+    stress_case("C4 shape 2 x 2^24 u64 fwd+inv", P62, 64, 24, 2)
+    stress_case("C5 shape 2^28 u64 fwd", P62, 64, 28, 1, ops=("fwd",))
+    stress_case("2^10 u32 fwd+inv", P30, 32, 10, 7)
 print(json.dumps(out))

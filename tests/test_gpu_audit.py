@@ -29,8 +29,21 @@ def _run(which):
 
 def test_no_range_violations_at_config_shapes():
     counts = _run("clean")
+    counts = {k: v for k, v in counts.items() if not k.startswith("STRESS")}
     assert len(counts) >= 8
     assert all(v == 0 for v in counts.values()), counts
+
+
+def test_race_stress_changes_nothing():
+    """Per-warp random delays at every round of every kernel (audit build's race stress; compute-sanitizer's
+    racecheck is closed on the pool): results bit-identical to the unstressed run, audit clean."""
+    counts = _run("stress")
+    assert len(counts) >= 6
+    for name, r in counts.items():
+        assert r["identical"] and r["violations"] == 0, (name, r)
+    # the delays really ran: the stressed C2 batch (thousands of rounds per SM) is slower
+    c2 = counts["STRESS C2 4096 x 2^12 u64 fwd+inv"]
+    assert c2["ms_stressed"] > 1.1 * c2["ms_plain"], c2
 
 
 def test_mutated_butterfly_is_reported():
