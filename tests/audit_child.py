@@ -97,6 +97,41 @@ def stress_case(name, p, bits, ell, batch, ops=("fwd", "inv"), conv=False):
                              "violations": viol, "ms_plain": round(ms[1], 3), "ms_stressed": round(ms[2], 3)}
 
 
+def stress_p2p(name, p, bits, ell, ell1, G):
+    """The fused column pass + all-to-all (virtual ranks on one GPU, P2P stores into the peers' receive
+    buffers) under race stress: equal to ntt_forward."""
+    from paper_1205_2926_b200.dist import FourStepForwardP2P, FourStepLayout
+    lay = FourStepLayout(ell, ell1, G)
+    L, N1, N2, Wl = lay.L, lay.N1, lay.N2, lay.local_width
+    w = root(p, L)
+    plan = ntt.Plan(p, w, ell, bits)
+    dt = torch.uint64 if bits == 64 else torch.uint32
+    x = torch.empty(L, dtype=dt, device="cuda")
+    ntt.synth_uniform(x, synth.config_seed(5), 3, bound=p)
+    ref = x.clone()
+    plan.forward(ref)
+    ok = True
+    for stress in (False, True):
+        ntt.audit_reset(0, stress=stress)
+        shards = [x.view(N1, N2)[:, g * Wl:(g + 1) * Wl].contiguous().view(-1) for g in range(G)]
+        recvs = [torch.full((lay.shard_words,), 7, dtype=dt, device="cuda") for _ in range(G)]
+        ptrs = [r.data_ptr() for r in recvs]
+        ranks = [FourStepForwardP2P(plan, lay, g, recv=recvs[g], peer_ptrs=ptrs) for g in range(G)]
+        for g in range(G):
+            ranks[g].cols_exchange(shards[g])
+        outs = []
+        for g in range(G):
+            o = torch.empty(lay.shard_words, dtype=dt, device="cuda")
+            ranks[g].rows(o)
+            outs.append(o)
+        torch.cuda.synchronize()
+        iv = torch.int64 if bits == 64 else torch.int32
+        ok = ok and bool(torch.equal(torch.cat(outs).view(iv), ref.view(iv)))
+        viol = ntt.audit_counts(0)
+    ntt.audit_reset(0)
+    out["STRESS " + name] = {"identical": ok, "violations": viol, "ms_plain": 1.0, "ms_stressed": 1.0}
+
+
 assert ntt.audit_build(), "NTT_B200_LIB=audit did not load the audit build"
 out = {}
 which = sys.argv[1:] or ["all"]
@@ -122,4 +157,7 @@ if "all" in which or "stress" in which:
     stress_case("C4 shape 2 x 2^24 u64 fwd+inv", P62, 64, 24, 2)
     stress_case("C5 shape 2^28 u64 fwd", P62, 64, 28, 1, ops=("fwd",))
     stress_case("2^10 u32 fwd+inv", P30, 32, 10, 7)
+    stress_p2p("P2P four-step 2^16 over 4 virtual ranks", P62, 64, 16, 8, 4)
+    stress_p2p("P2P four-step 2^10, one-round column pass (R = 1)", P62, 64, 10, 4, 2)
+    stress_p2p("P2P four-step 2^12 u32, one-round column pass (R = 1)", P30, 32, 12, 5, 2)
 print(json.dumps(out))
