@@ -140,6 +140,9 @@ struct SplitStage {
   const CUtensorMap* map_a;  // forward with PW: 128-byte rows of a (a-hat in, c-hat out)
 };
 
+#ifndef NTT_SPLIT_DRAIN  // plain K = 2 forward: buffer chunks issued per drained store group, after the
+#define NTT_SPLIT_DRAIN 1  // stage-1 X barrier (0: all at the transform's start after the whole store read)
+#endif
 #ifndef NTT_SPLIT_NX  // spare staging slots of the K = 2 forward (A/B on one box, round 2: 2 slots
 #define NTT_SPLIT_NX 2    // beat 3 -- C4 row pass 10.68 -> 10.61 ms, C3 2.537 -> 2.523 ms -- the smaller
 #endif                    // shared-memory footprint leaves more L1 to the twiddle loads)
@@ -172,6 +175,18 @@ template <class W, int LOGQ, int LE> struct SplitFwd {
       tma_load_2d(dst + hf * HALF, map, 0, (int)((b * 2 + hf) * (size_t)ROWS_BLK) + k * BOXR, bar);
   }
 };
+
+// Chunk NX + i of transform b into buffer slot i once the previous transform's bulk store group i has
+// read it (NTT_SPLIT_DRAIN; the store commits one group per chunk slot).
+template <class W, int LOGQ, int LE, int I = 0>
+__device__ __forceinline__ void split_issue_drained(const CUtensorMap* map, size_t b, uint32_t sbase) {
+  using F = SplitFwd<W, LOGQ, LE>;
+  if constexpr (I < F::NB) {
+    bulk_wait_read<F::NB - 1 - I>();
+    F::issue(map, b, F::NX + I, sbase);
+    split_issue_drained<W, LOGQ, LE, I + 1>(map, b, sbase);
+  }
+}
 
 // Stage 1 of the forward from the staged chunks: CTA 0 keeps sums, CTA 1 twiddled differences.
 // SCALE (forward with the pointwise product): stage 1 also multiplies by K = beta L^{-1} -- CTA 0's
@@ -219,9 +234,16 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
     if (k == F::NX - 1) {  // X slots consumed: the late chunks reuse them
       fence_proxy_async_smem();
       __syncthreads();
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
+        if constexpr (NTT_SPLIT_DRAIN) {
+          // the buffer chunks NX..NX+NB-1, each as soon as the previous transform's store (one bulk
+          // group per chunk slot, committed in slot order) has read that slot; the other warps go on
+          // to wait for chunk NX's data instead of for this thread
+          split_issue_drained<W, LOGQ, LE>(st.map, st.b, sbase);
+        }
 #pragma unroll
         for (int kk = F::NX + F::NB; kk < F::NCH; ++kk) F::issue(st.map, st.b, kk, sbase);
+      }
     }
   }
   // (the X slots take the next transform's first chunks at the first round's exchange barrier)
@@ -419,9 +441,14 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         constexpr int BOX = (K == 2) ? SplitFwd<W, LOGQ, LE>::BOXR : (ROWS < 256 ? ROWS : 256);
         const int row0 = (int)((st.b * K + (size_t)rank) * (size_t)ROWS);
         const CUtensorMap* omap = PW ? st.map_a : st.map;
+        // K = 2 with NTT_SPLIT_DRAIN: one bulk group per staging-chunk slot of the buffer, in slot order,
+        // so the next transform's chunks can follow the store's reads slot by slot
+        constexpr int PERG = (K == 2 && NTT_SPLIT_DRAIN) ? (int)(SplitFwd<W, LOGQ, LE>::CH / (BOX * 128)) : ROWS / BOX;
 #pragma unroll
-        for (int bx = 0; bx < ROWS / BOX; ++bx) tma_store_2d(omap, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
-        bulk_commit();
+        for (int bx = 0; bx < ROWS / BOX; ++bx) {
+          tma_store_2d(omap, 0, row0 + bx * BOX, smem_u32(sm) + bx * BOX * 128);
+          if ((bx + 1) % PERG == 0) bulk_commit();
+        }
       }
     } else {
       // stages s..1 across the cluster through DSMEM (Algorithm 4)
@@ -604,7 +631,7 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     st.phase = it & 1;
     st.b = b;
     st.next_b = b + groups;
-    if constexpr (FWD_TMA) {
+    if constexpr (FWD_TMA && !NTT_SPLIT_DRAIN) {
       // the Q-word buffer takes chunks NX..NX+3 once the previous transform's store has read it
       if (threadIdx.x == 0) {
         bulk_wait_read0();
