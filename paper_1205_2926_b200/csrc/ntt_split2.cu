@@ -116,9 +116,10 @@ template <class W, int LOGQ, int LE, int K, bool INV, bool PW> struct SplitStagi
   // shrink the L1 carveout made the fused convolution slower: 3 slots +20%, 2 +6%, 1 +2%)
   static constexpr int NX = (K == 2 && NCH == 4 && !PW) ? 3 : 0;
   static constexpr uint32_t X_OFF = BYTES, BAR_OFF = X_OFF + NX * CH;
-  static constexpr size_t SMEM = BAR_OFF + 8 * NCH;
+  static constexpr size_t SMEM = BAR_OFF + 8 * NCH + 8;  // + the K = 2 push mbarrier (st.async epilogue)
   __device__ static constexpr uint32_t slot(int k) { return k < NX ? X_OFF + k * CH : k * CH; }
   __device__ static uint32_t bar(uint32_t sbase, int k) { return sbase + BAR_OFF + 8 * k; }
+  __device__ static uint32_t push_bar(uint32_t sbase) { return sbase + BAR_OFF + 8 * NCH; }
   // chunks [k0, k1) of this CTA's block of transform b
   __device__ static void issue(const CUtensorMap* map, size_t b, int rank, int k0, int k1, uint32_t sbase) {
     const int row0 = (int)((b * K + (size_t)rank) * (size_t)ROWS);
@@ -142,6 +143,9 @@ struct SplitStage {
 
 #ifndef NTT_SPLIT_DRAIN  // plain K = 2 forward: buffer chunks issued per drained store group, after the
 #define NTT_SPLIT_DRAIN 1  // stage-1 X barrier (0: all at the transform's start after the whole store read)
+#endif
+#ifndef NTT_SPLIT_STASYNC  // K = 2 inverse: the cross-CTA push by st.async + mbarrier (0: remote stores +
+#define NTT_SPLIT_STASYNC 1  // cluster.sync, round 2's form)
 #endif
 #ifndef NTT_SPLIT_NX  // spare staging slots of the K = 2 forward (A/B on one box, round 2: 2 slots
 #define NTT_SPLIT_NX 2    // beat 3 -- C4 row pass 10.68 -> 10.61 ms, C3 2.537 -> 2.523 ms -- the smaller
@@ -464,15 +468,30 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         // the other CTA has consumed its round inputs (relaxed: this CTA's inputs are consumed too,
         // the round's arithmetic used them) before this CTA's stores overwrite its buffer
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-        W* other = cluster.map_shared_rank(sm, rank ^ 1);
-        if (rank == 0) {
+        if constexpr (NTT_SPLIT_STASYNC) {
+          // asynchronous remote stores that count their bytes on the receiver's push mbarrier (armed
+          // for H2 D words once per transform by its thread 0): the receiver waits on its own mbarrier,
+          // with no cluster barrier and none of cluster.sync()'s release / acquire fences
+          using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
+          const uint32_t pbar = St::push_bar(smem_u32(sm));
+          if (threadIdx.x == 0) mbar_expect_tx(pbar, (uint32_t)(H2 * D * sizeof(W)));
+          const uint32_t rbase = mapa_u32(smem_u32(sm + t), (uint32_t)(rank ^ 1));
+          const uint32_t rbar = mapa_u32(pbar, (uint32_t)(rank ^ 1));
 #pragma unroll
-          for (int h = 0; h < H2; ++h) other[h * D + t] = v[H2 + h];
+          for (int h = 0; h < H2; ++h)
+            st_async(rbase + (uint32_t)(h * D * sizeof(W)), rank == 0 ? v[H2 + h] : v[h], rbar);
+          mbar_wait(pbar, st.phase);  // the other CTA's half has landed
         } else {
+          W* other = cluster.map_shared_rank(sm, rank ^ 1);
+          if (rank == 0) {
 #pragma unroll
-          for (int h = 0; h < H2; ++h) other[h * D + t] = v[h];
+            for (int h = 0; h < H2; ++h) other[h * D + t] = v[H2 + h];
+          } else {
+#pragma unroll
+            for (int h = 0; h < H2; ++h) other[h * D + t] = v[h];
+          }
+          cluster.sync();  // the pushed halves are visible
         }
-        cluster.sync();  // the pushed halves are visible
         const int off = stage_off(LOGL, 1);
         constexpr int U = sizeof(W) == 4 ? 8 : 4;
         static_assert(H2 % U == 0, "whole groups");
@@ -604,9 +623,13 @@ __global__ void __launch_bounds__(SplitShape<LOGQ, LE, K, (int)sizeof(W)>::T,
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < St::NCH; ++k) mbar_init(St::bar(smem_u32(sm), k), 1);
+      if constexpr (K == 2 && NTT_SPLIT_STASYNC) mbar_init(St::push_bar(smem_u32(sm)), 1);
       fence_mbar_init();
     }
-    __syncthreads();
+    // the partner's st.async pushes signal this CTA's push mbarrier: its initialisation must be
+    // visible cluster-wide first (the epilogue's own cluster barrier is a relaxed one)
+    if constexpr (K == 2 && NTT_SPLIT_STASYNC) cluster.sync();
+    else __syncthreads();
   }
   constexpr bool FWD_TMA = !INV && K == 2;
   using F = SplitFwd<W, LOGQ, LE>;
