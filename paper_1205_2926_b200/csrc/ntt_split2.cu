@@ -147,6 +147,8 @@ struct SplitStage {
 #ifndef NTT_SPLIT_STASYNC  // K = 2 inverse: the cross-CTA push by st.async + mbarrier (0: remote stores +
 #define NTT_SPLIT_STASYNC 1  // cluster.sync, round 2's form)
 #endif
+// Timing-only experiment hooks (results wrong; DESIGN.md §7 removal bounds): NTT_XP_NOEXCH drops the
+// exchanges' shared-memory traffic, NTT_XP_NOWAIT the stage-1 data waits of the K = 2 forward.
 #ifndef NTT_SPLIT_NX  // spare staging slots of the K = 2 forward (A/B on one box, round 2: 2 slots
 #define NTT_SPLIT_NX 2    // beat 3 -- C4 row pass 10.68 -> 10.61 ms, C3 2.537 -> 2.523 ms -- the smaller
 #endif                    // shared-memory footprint leaves more L1 to the twiddle loads)
@@ -207,7 +209,9 @@ __device__ __forceinline__ void split_fwd_stage1(W* v, const W* sm, int t, const
   NTT_AUDIT_STRESS();
 #pragma unroll
   for (int k = 0; k < F::NCH; ++k) {
+#ifndef NTT_XP_NOWAIT
     mbar_wait(sbase + F::BAR_OFF + 8 * k, st.phase);
+#endif
     const W* lo = reinterpret_cast<const W*>(base + F::slot(k));
     const W* hi = reinterpret_cast<const W*>(base + F::slot(k) + F::HALF);
 #pragma unroll
@@ -379,9 +383,17 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       for (int h = 0; h < S; ++h) {
         if constexpr (REMAP) {
           constexpr int PER = 16 / (int)sizeof(W);
+#ifndef NTT_XP_NOEXCH
           if (h % PER == 0) unpack16<W>(lds128(sm + xswz<W>(blk[q] * B + h)), v + q * S + h);
+#else
+          v[q * S + h] += (W)(blk[q] * B + h);
+#endif
         } else {
+#ifndef NTT_XP_NOEXCH
           v[q * S + h] = sm[sswz<W>(blk[q] * B + h * D + c[q])];
+#else
+          v[q * S + h] += (W)(blk[q] * B + h * D + c[q]);
+#endif
         }
       }
   }
@@ -594,7 +606,11 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
 #pragma unroll
       for (int h = 0; h < S; ++h) {
         const int i = blk[q] * B + h * D + c[q];
+#ifndef NTT_XP_NOEXCH
         sm[NEXT_REMAP ? xswz<W>(i) : sswz<W>(i)] = v[q * S + h];
+#else
+        if (i == 0) sm[0] = v[q * S + h];
+#endif
       }
     if constexpr (WL) __syncwarp();
     else __syncthreads();
