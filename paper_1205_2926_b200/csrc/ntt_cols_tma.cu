@@ -5,11 +5,11 @@
 // runs length-N NTTs (Algorithm 1, Algorithm 3 / 4 butterflies) down the
 // C columns and applies the four-step twiddle omega^{c rev(r)} (forward: after,
 // inverse: omega^{-c rev(r)} before).  Here the tile comes in through one 3-D TMA
-// load (cp.async.bulk.tensor.3d, SWIZZLE_128B: 16-byte chunk ^= row mod 8) into one
+// load (cp.async.bulk.tensor.3d; plain 128-byte rows, see NTT_COLS_SWZ) into one
 // of two shared-memory buffers while the CTA computes the other, and leaves through
 // a TMA bulk tensor store, so HBM latency is off the critical path of the strided
 // (2^9-2^19-word stride) column accesses.  Every round of a warp touches whole
-// 128-byte smem rows, so the swizzled layout is bank-conflict free.
+// 128-byte smem rows, so the plain row layout is bank-conflict free.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -24,6 +24,18 @@
 #include "tma.cuh"
 
 namespace nttb {
+
+// Tile layout: plain 128-byte rows (NTT_COLS_SWZ 0, default) or the TMA 128-byte swizzle (1, round 2's
+// form).  Every shared-memory access of this kernel is one warp (u32) or one half-warp (u64) reading or
+// writing one whole 128-byte row, so the plain layout is conflict-free too, and its addresses are a
+// per-thread base plus compile-time row offsets (no XOR per access).
+#ifndef NTT_COLS_SWZ
+#define NTT_COLS_SWZ 0
+#endif
+template <class W> __device__ __forceinline__ int cswz(int i) {
+  if constexpr (NTT_COLS_SWZ) return tswz<W>(i);
+  else return i;
+}
 
 template <class W, int LOGN, int LE> struct ColsTmaShape {
   static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E, C = 128 / (int)sizeof(W), THREADS = T * C;
@@ -78,7 +90,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      v[q * S + h] = sm[tswz<W>(row * C + cc)];
+      v[q * S + h] = sm[cswz<W>(row * C + cc)];
     }
   if constexpr (INV && first) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
     if (prm.twiddle) {
@@ -146,7 +158,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      sm[tswz<W>(row * C + cc)] = v[q * S + h];  // each thread rewrites exactly the positions it read
+      sm[cswz<W>(row * C + cc)] = v[q * S + h];  // each thread rewrites exactly the positions it read
     }
   if constexpr (!last) {
     __syncthreads();
@@ -219,7 +231,8 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
       constexpr int PER = 16 / (int)sizeof(W);
       for (int i = threadIdx.x; i < Sh::N * 8; i += Sh::THREADS) {
         const int row = i >> 3, k = i & 7;
-        const uint4 val = lds128(reinterpret_cast<const unsigned char*>(sm) + row * 128 + ((k ^ (row & 7)) << 4));
+        const uint4 val = lds128(reinterpret_cast<const unsigned char*>(sm) + row * 128 +
+                                 ((NTT_COLS_SWZ ? (k ^ (row & 7)) : k) << 4));
         const uint64_t r = bq * Sh::N + (uint64_t)row;  // global row (the last pass's blocks are N rows x N2/G)
         W* dst = reinterpret_cast<W*>(select_peer(prm.peer, (uint32_t)(r >> prm.log_rows_rank))) +
                  ((uint64_t)prm.src_rank << (prm.log_rows_rank + prm.log_local_w)) +
@@ -278,7 +291,8 @@ static cudaError_t run_cols_tma_k(void* x, const ColsParams& prm, const DevTable
   cuuint32_t box[3] = {(cuuint32_t)Sh::C, (cuuint32_t)Sh::BOX_ROWS, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&map, sizeof(W) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, x, dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    NTT_COLS_SWZ ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                     cols_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   auto kern = k_cols_tma<W, LOGN, LE, INV, PLO1, P2P, TWM, BF>;
