@@ -32,6 +32,9 @@ namespace nttb {
 #ifndef NTT_COLS_SWZ
 #define NTT_COLS_SWZ 0
 #endif
+#ifndef NTT_COLS_MIDBAR  // 1: a CTA barrier between a round's butterflies and its write-back (round 2's form)
+#define NTT_COLS_MIDBAR 0
+#endif
 template <class W> __device__ __forceinline__ int cswz(int i) {
   if constexpr (NTT_COLS_SWZ) return tswz<W>(i);
   else return i;
@@ -111,7 +114,9 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
   if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF, last>(v, c, tw, m);
   else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
   if constexpr (!last) {
-    __syncthreads();
+    // (no CTA barrier here: a round writes back exactly the positions each thread read, and the other
+    // buffer is free since the previous tile's closing barrier; only thread 0's own store group matters)
+    if constexpr (NTT_COLS_MIDBAR) __syncthreads();
     if (prefetch && threadIdx.x == 0) {  // the other buffer's store has been issued: reuse it once read
       bulk_wait_read0();
       cols_tma_issue<W, LOGN, LE, TWM == 2>(map, next_tile, prm, next_buf, next_bar);
@@ -240,9 +245,10 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
         *reinterpret_cast<uint4*>(dst) = val;
       }
       fence_proxy_async_smem();  // these generic reads precede the buffer's next TMA load
-      // with one round (R == 1) the next iteration's prefetch into this buffer is issued at the top of
-      // the loop, not behind a round's CTA barrier: every warp must have finished reading it first
-      if constexpr (Sh::R == 1) __syncthreads();
+      // the next iteration's prefetch into this buffer (at the top of the loop when R == 1, else in the
+      // next tile's first round, which has no CTA barrier before it): every warp must have finished
+      // reading it first
+      if constexpr (Sh::R == 1 || !NTT_COLS_MIDBAR) __syncthreads();
     } else if (threadIdx.x == 0) {
       const int c0 = (int)cg * Sh::C;
 #pragma unroll
