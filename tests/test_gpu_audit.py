@@ -41,9 +41,11 @@ def test_race_stress_changes_nothing():
     assert len(counts) >= 6
     for name, r in counts.items():
         assert r["identical"] and r["violations"] == 0, (name, r)
-    # the delays really ran: the stressed C2 batch (thousands of rounds per SM) is slower
-    c2 = counts["STRESS C2 4096 x 2^12 u64 fwd+inv"]
-    assert c2["ms_stressed"] > 1.1 * c2["ms_plain"], c2
+    # the delays really ran: the stressed runs together are slower (summed over the timed cases, so one
+    # case's cold first run or a kernel whose warps absorb the delays cannot hide it)
+    timed = [r for name, r in counts.items() if "P2P" not in name]
+    plain, stressed = sum(r["ms_plain"] for r in timed), sum(r["ms_stressed"] for r in timed)
+    assert stressed > 1.1 * plain, counts
 
 
 def test_mutated_butterfly_is_reported():
