@@ -83,10 +83,19 @@ template <int LOGQ, int LE, int WB, int ra, int rb> __host__ __device__ constexp
   // (u64 only: measured u64 2^15 inverse -6.3 %, forward -0.1 %; for u32 the plain exchange made C3 +2.8 %)
   return NTT_SPLIT_PLAINX && WB == 8 && T % 32 == 0 && Da >= ROWW && Db >= ROWW;
 }
+// NTT_SPLIT_REMAP2 (default): lane l of warp w takes the remapped round's groups 32 G w + 32 q + l (one
+// 128-byte row each for u64) instead of G consecutive ones, still inside the warp's 32 E words; the
+// exchange then uses the TMA swizzle itself (chunk ^= row mod 8), so the round's 16-byte reads and the
+// epilogue's 16-byte stores into the TMA-swizzled buffer cover 8 chunk positions per 8 lanes: no 2-way
+// conflict on the epilogue's STS.128 (with G consecutive rows per thread, row mod 8 took 4 values).
+#ifndef NTT_SPLIT_REMAP2
+#define NTT_SPLIT_REMAP2 1
+#endif
 template <class W> __device__ __forceinline__ int xswz(int i) {  // 16-byte chunk ^= (row / 2) mod 8
   constexpr int CS = sizeof(W) == 8 ? 1 : 2;  // log2 words per chunk
   constexpr int RS = sizeof(W) == 8 ? 4 : 5;  // log2 words per 128-byte row
-  return i ^ ((((i >> RS) >> 1) & 7) << CS);
+  if constexpr (NTT_SPLIT_REMAP2) return i ^ (((i >> RS) & 7) << CS);
+  else return i ^ ((((i >> RS) >> 1) & 7) << CS);
 }
 
 template <int LOGQ, int LE, int K, int WB = 8> struct SplitShape {
@@ -292,7 +301,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
   int c[G], blk[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) {
-    const int g = REMAP ? t * G + q : t + Sh::T * q;
+    const int g = REMAP ? (NTT_SPLIT_REMAP2 ? (t >> 5) * (32 * G) + 32 * q + (t & 31) : t * G + q) : t + Sh::T * q;
     blk[q] = g / D;
     c[q] = g % D;
   }
