@@ -91,6 +91,25 @@ template <int LOGQ, int LE, int WB, int ra, int rb> __host__ __device__ constexp
 #ifndef NTT_SPLIT_REMAP2
 #define NTT_SPLIT_REMAP2 1
 #endif
+// u32 forward (NTT_SPLIT_RUNV): the exchange into the last round, whose groups are one 32-word run per
+// thread (G = 1, D = 1) written by a round with D >= 32, uses the TMA chunk swizzle (16-byte chunk ^=
+// row mod 8) instead of the element swizzle, so the last round reads its run with 8 16-byte loads
+// instead of 32 4-byte ones (conflict-free on both sides: a warp writes one whole row per store, and the
+// 8 lanes of a quarter-warp read 8 distinct chunk positions).
+#ifndef NTT_SPLIT_RUNV
+#define NTT_SPLIT_RUNV 1
+#endif
+template <int LOGQ, int LE, int WB, int r> __host__ __device__ constexpr bool runv_round() {
+  using RC = Rounds<LOGQ, LE>;
+  constexpr int Q = 1 << LOGQ, E = 1 << LE, T = Q >> LE;
+  if constexpr (!NTT_SPLIT_RUNV || WB != 4 || r != RC::R - 1 || r == 0) {
+    return false;
+  } else {
+    constexpr int S = 1 << RC::sr(r), D = Q >> (RC::level(r) + RC::sr(r));
+    constexpr int Dp = Q >> (RC::level(r - 1) + RC::sr(r - 1));
+    return S == E && D == 1 && Dp >= 32 && T % 32 == 0;
+  }
+}
 template <class W> __device__ __forceinline__ int xswz(int i) {  // 16-byte chunk ^= (row / 2) mod 8
   constexpr int CS = sizeof(W) == 8 ? 1 : 2;  // log2 words per chunk
   constexpr int RS = sizeof(W) == 8 ? 4 : 5;  // log2 words per 128-byte row
@@ -298,6 +317,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
       BF == 5 ? reinterpret_cast<const TwPair<W>*>(reinterpret_cast<const W*>(tw_full) + stage_off(LOGL, SS + 1))
               : tw_full + stage_off(LOGL, SS + 1);
   constexpr bool REMAP = !INV && split_remap_last<LOGQ, LE, r>();  // this round: remapped groups
+  constexpr bool RUNV = !INV && runv_round<LOGQ, LE, (int)sizeof(W), r>();  // this round: 16-byte run reads
   int c[G], blk[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) {
@@ -404,10 +424,11 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     for (int q = 0; q < G; ++q)
 #pragma unroll
       for (int h = 0; h < S; ++h) {
-        if constexpr (REMAP) {
+        if constexpr (REMAP || RUNV) {
           constexpr int PER = 16 / (int)sizeof(W);
 #ifndef NTT_XP_NOEXCH
-          if (h % PER == 0) unpack16<W>(lds128(sm + xswz<W>(blk[q] * B + h)), v + q * S + h);
+          if (h % PER == 0)
+            unpack16<W>(lds128(sm + (RUNV ? tswz<W>(blk[q] * B + h) : xswz<W>(blk[q] * B + h))), v + q * S + h);
 #else
           v[q * S + h] += (W)(blk[q] * B + h);
 #endif
@@ -608,6 +629,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
     // barrier): it rides on the first exchange, or on the second when the first is warp-local.
     constexpr int nr_ = INV ? r - 1 : r + 1;
     constexpr bool NEXT_REMAP = !INV && split_remap_last<LOGQ, LE, nr_>();  // writes into the remapped round
+    constexpr bool NEXT_RUNV = !INV && runv_round<LOGQ, LE, (int)sizeof(W), nr_>();
     constexpr bool WL = (warp_local_exchange<LOGQ, LE, r, nr_>() || NEXT_REMAP) && !(INV && Sh::R < 3);
     constexpr bool FIRST_WL = INV && Sh::R >= 3 && warp_local_exchange<LOGQ, LE, Sh::R - 1, Sh::R - 2>();
     using St = SplitStaging<W, LOGQ, LE, K, INV, PW>;
@@ -634,7 +656,7 @@ __device__ __forceinline__ void split_round(W* v, W* __restrict__ xb, W* sm, int
         const int i = blk[q] * B + h * D + c[q];
 #ifndef NTT_XP_NOEXCH
         constexpr bool PLAIN = plain_exchange<LOGQ, LE, (int)sizeof(W), r, nr_>();
-        sm[NEXT_REMAP ? xswz<W>(i) : (PLAIN ? i : sswz<W>(i))] = v[q * S + h];
+        sm[NEXT_REMAP ? xswz<W>(i) : (NEXT_RUNV ? tswz<W>(i) : (PLAIN ? i : sswz<W>(i)))] = v[q * S + h];
 #else
         if (i == 0) sm[0] = v[q * S + h];
 #endif
