@@ -63,6 +63,9 @@ __device__ __forceinline__ W fourstep_twiddle_bf(W val, uint32_t e, uint32_t H, 
   }
 }
 
+#ifndef NTT_COLS_POW2  // tile coordinates by shifts when the block count is a power of two
+#define NTT_COLS_POW2 1
+#endif
 // Block index and column group of a column-pass tile (ColsParams::bmajor: DESIGN.md §5).
 // BM: the kernel supports the block-major order (only the twiddle-matrix instantiations do).
 template <bool BM = true>
@@ -72,8 +75,15 @@ __device__ __forceinline__ void cols_tile_coords(uint64_t tile, const ColsParams
     cg = (uint32_t)(tile & ((1ull << prm.log_colgroups) - 1));
   } else {
     const uint64_t nblk = prm.n_tiles >> prm.log_colgroups, rest = tile >> prm.log_cgi;
-    bq = rest % nblk;
-    cg = ((uint32_t)(rest / nblk) << prm.log_cgi) | (uint32_t)(tile & ((1u << prm.log_cgi) - 1));
+    uint64_t qt;
+    if (NTT_COLS_POW2 && (nblk & (nblk - 1)) == 0) {  // a power-of-two count of blocks (C4, C5): no division
+      bq = rest & (nblk - 1);
+      qt = rest >> (__ffsll((long long)nblk) - 1);
+    } else {
+      bq = rest % nblk;
+      qt = rest / nblk;
+    }
+    cg = ((uint32_t)qt << prm.log_cgi) | (uint32_t)(tile & ((1u << prm.log_cgi) - 1));
   }
 }
 

@@ -40,8 +40,17 @@ template <class W> __device__ __forceinline__ int cswz(int i) {
   else return i;
 }
 
+// NTT_COLS_NC2: C4's u64 2^9 column pass gives each thread two adjacent columns (NC = 2: 16-byte shared-memory
+// accesses, and every stage twiddle it loads serves both columns' butterflies), 512 threads per tile
+#ifndef NTT_COLS_NC2
+#define NTT_COLS_NC2 1
+#endif
+template <class W, int LOGN, int LE> struct ColsNC {
+  static constexpr int value = (NTT_COLS_NC2 && !NTT_COLS_SWZ && sizeof(W) == 8 && LOGN == 9 && LE == 3) ? 2 : 1;
+};
 template <class W, int LOGN, int LE> struct ColsTmaShape {
-  static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E, C = 128 / (int)sizeof(W), THREADS = T * C;
+  static constexpr int NC = ColsNC<W, LOGN, LE>::value;  // adjacent columns per thread
+  static constexpr int N = 1 << LOGN, E = 1 << LE, T = N / E, C = 128 / (int)sizeof(W), THREADS = T * C / NC;
   static constexpr int TILE_BYTES = N * 128;
   static constexpr int BOX_ROWS = N < 256 ? N : 256;
   static constexpr int BOXES = N / BOX_ROWS;
@@ -66,7 +75,7 @@ __device__ __forceinline__ void cols_tma_issue(const CUtensorMap* map, uint64_t 
 }
 
 template <class W, int LOGN, int LE, bool INV, bool PLO1, int TWM, int BF, int r>
-__device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint32_t cglob, const ColsParams& prm,
+__device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, const uint32_t (&cgl)[2], const ColsParams& prm,
                                                const TwPair<W>* __restrict__ tw, const TwPair<W>* __restrict__ fa,
                                                const TwPair<W>* __restrict__ fb, const TwPair<W>* __restrict__ fm,
                                                const Mod<W>& m, const CUtensorMap* map, uint64_t next_tile,
@@ -78,7 +87,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
   constexpr int SR = RC::sr(r), LEVEL = RC::level(r);
   constexpr int S = 1 << SR, G = Sh::E >> SR;
   constexpr int D = Sh::N >> (LEVEL + SR), B = Sh::N >> LEVEL;
-  constexpr int C = Sh::C;
+  constexpr int C = Sh::C, NC = Sh::NC, E = Sh::E;
   int c[G], blk[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) {
@@ -86,6 +95,7 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
     blk[q] = g / D;
     c[q] = g % D;
   }
+  // column k < NC of this thread (cc + k) keeps its words at v[k E + q S + h]
   constexpr bool first = INV ? (r == Sh::R - 1) : (r == 0);
   constexpr bool last = INV ? (r == 0) : (r == Sh::R - 1);
 #pragma unroll
@@ -93,26 +103,35 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      v[q * S + h] = sm[cswz<W>(row * C + cc)];
+      if constexpr (NC == 2) {
+        const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(sm + row * C + cc);
+        v[q * S + h] = (W)u.x;
+        v[E + q * S + h] = (W)u.y;
+      } else {
+        v[q * S + h] = sm[cswz<W>(row * C + cc)];
+      }
     }
   if constexpr (INV && first) {  // four-step twiddle omega^{-c rev(r)} before the inverse column NTT
     if (prm.twiddle) {
       const uint32_t emask = (uint32_t)((((uint64_t)1 << prm.ell)) - 1);
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
         for (int h = 0; h < S; ++h) {
           const int row = blk[q] * B + h * D + c[q];
           const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
-          const uint32_t e = (cglob * rv) << prm.log_tw_mul;
-          v[q * S + h] = fourstep_twiddle_ct<W, PLO1, TWM != 0>(v[q * S + h], (0u - e) & emask, prm.H, fa, fb, m);
+          const uint32_t e = (cgl[k] * rv) << prm.log_tw_mul;
+          v[k * E + q * S + h] =
+              fourstep_twiddle_ct<W, PLO1, TWM != 0>(v[k * E + q * S + h], (0u - e) & emask, prm.H, fa, fb, m);
         }
     }
   }
   // forward column passes multiply every output by the four-step twiddle next: the last stage's W = 1
   // butterflies skip their corrections (LAZY_LAST); prm.twiddle is 1 for every forward column pass
-  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF, last>(v, c, tw, m);
-  else dit_round<W, LOGN, SR, LEVEL, G, PLO1>(v, c, tw, m);
+  if constexpr (!INV) dif_round<W, LOGN, SR, LEVEL, G, PLO1, BF, last, NC>(v, c, tw, m);
+  else dit_round<W, LOGN, SR, LEVEL, G, PLO1, NC>(v, c, tw, m);
   if constexpr (!last) {
     // (no CTA barrier here: a round writes back exactly the positions each thread read, and the other
     // buffer is free since the previous tile's closing barrier; only thread 0's own store group matters)
@@ -126,36 +145,38 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
     if constexpr (!INV) {  // four-step twiddle omega^{c rev(r)} after the forward column NTT (every forward
       {                    // column pass has one; the lazy last stage above relies on it)
 #pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
         for (int q = 0; q < G; ++q)
 #pragma unroll
           for (int h = 0; h < S; ++h) {
             const int row = blk[q] * B + h * D + c[q];
+            W& x = v[k * E + q * S + h];
             if constexpr (TWM == 2) {  // twiddle matrix: M[row][c] = omega_B^{c rev(row)}, one product
               W w, wp;
-              ldtw_bf<W, BF>(fm, ((uint32_t)row << prm.log_S) + cglob, w, wp);
-              v[q * S + h] = twiddle_mul<W, PLO1, BF>(v[q * S + h], w, wp, m);
+              ldtw_bf<W, BF>(fm, ((uint32_t)row << prm.log_S) + cgl[k], w, wp);
+              x = twiddle_mul<W, PLO1, BF>(x, w, wp, m);
             } else {
               const uint32_t rv = __brev((uint32_t)row) >> (32 - LOGN);
-              v[q * S + h] = fourstep_twiddle_bf<W, PLO1, TWM == 1, BF>(v[q * S + h], (cglob * rv) << prm.log_tw_mul,
-                                                                         prm.H, fa, fb, m);
+              x = fourstep_twiddle_bf<W, PLO1, TWM == 1, BF>(x, (cgl[k] * rv) << prm.log_tw_mul, prm.H, fa, fb, m);
             }
           }
       }
       if (prm.normalize) {
 #pragma unroll
-        for (int i = 0; i < Sh::E; ++i) v[i] = norm2<W>(v[i], m.p);
+        for (int i = 0; i < NC * E; ++i) v[i] = norm2<W>(v[i], m.p);
       }
     } else {
       if (prm.normalize) {
 #pragma unroll
-        for (int i = 0; i < Sh::E; ++i) v[i] = norm4<W>(v[i], m.p, m.p2);
+        for (int i = 0; i < NC * E; ++i) v[i] = norm4<W>(v[i], m.p, m.p2);
       }
     }
   }
 #ifdef NTT_RANGE_AUDIT
   if constexpr (last) {  // the buffer this pass leaves for the next one (or the final output)
 #pragma unroll
-    for (int i = 0; i < Sh::E; ++i) NTT_AUDIT(v[i], prm.normalize ? m.p : (INV ? 2 * m.p2 : m.p2));
+    for (int i = 0; i < NC * E; ++i) NTT_AUDIT(v[i], prm.normalize ? m.p : (INV ? 2 * m.p2 : m.p2));
   }
 #endif
 #pragma unroll
@@ -163,12 +184,17 @@ __device__ __forceinline__ void cols_tma_round(W* v, W* sm, int t, int cc, uint3
 #pragma unroll
     for (int h = 0; h < S; ++h) {
       const int row = blk[q] * B + h * D + c[q];
-      sm[cswz<W>(row * C + cc)] = v[q * S + h];  // each thread rewrites exactly the positions it read
+      if constexpr (NC == 2) {  // each thread rewrites exactly the positions it read
+        *reinterpret_cast<ulonglong2*>(sm + row * C + cc) =
+            make_ulonglong2((unsigned long long)v[q * S + h], (unsigned long long)v[E + q * S + h]);
+      } else {
+        sm[cswz<W>(row * C + cc)] = v[q * S + h];  // each thread rewrites exactly the positions it read
+      }
     }
   if constexpr (!last) {
     __syncthreads();
     constexpr int nr = INV ? r - 1 : r + 1;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, nr>(v, sm, t, cc, cglob, prm, tw, fa, fb, fm, m, map, next_tile,
+    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, nr>(v, sm, t, cc, cgl, prm, tw, fa, fb, fm, m, map, next_tile,
                                                     next_buf, next_bar, false);
   }
 }
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
   const uint32_t buf0 = smem_u32(base), bar0 = smem_u32(&bars[0]);
   auto buf_of = [&](int i) { return buf0 + (uint32_t)i * (uint32_t)Sh::TILE_BYTES; };
   auto bar_of = [&](int i) { return bar0 + (uint32_t)i * 8u; };
-  const int cc = threadIdx.x % Sh::C, t = threadIdx.x / Sh::C;
+  const int cc = (threadIdx.x % (Sh::C / Sh::NC)) * Sh::NC, t = threadIdx.x / (Sh::C / Sh::NC);
   const Mod<W> m = make_mod<W>(p);
   if (threadIdx.x == 0) {
     mbar_init(bar_of(0), 1);
@@ -207,7 +233,7 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     }
   }
   if (threadIdx.x == 0 && tile < tend) cols_tma_issue<W, LOGN, LE, TWM == 2>(&tmap, tile, prm, buf_of(0), bar_of(0));
-  W v[Sh::E];
+  W v[Sh::E * Sh::NC];
   for (uint32_t it = 0; tile < tend; ++it, tile += tstep) {
     const int cur = it & 1;
     const uint64_t next = tile + tstep;
@@ -221,10 +247,12 @@ __global__ void __launch_bounds__(ColsTmaShape<W, LOGN, LE>::THREADS, ColsTmaSha
     uint64_t bq;
     uint32_t cg;
     cols_tile_coords<TWM == 2>(tile, prm, bq, cg);
-    const uint32_t cglob = cols_global_column(cg * Sh::C + cc, prm);
+    uint32_t cgl[2];
+    cgl[0] = cols_global_column(cg * Sh::C + cc, prm);
+    cgl[1] = Sh::NC == 2 ? cols_global_column(cg * Sh::C + cc + 1, prm) : cgl[0];
     W* sm = reinterpret_cast<W*>(base + (size_t)cur * Sh::TILE_BYTES);
     constexpr int r0 = INV ? Sh::R - 1 : 0;
-    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, r0>(v, sm, t, cc, cglob, prm, tw, fa, fb, fm, m, &tmap, next,
+    cols_tma_round<W, LOGN, LE, INV, PLO1, TWM, BF, r0>(v, sm, t, cc, cgl, prm, tw, fa, fb, fm, m, &tmap, next,
                                                     buf_of(cur ^ 1), bar_of(cur ^ 1), Sh::R > 1 && next < tend);
     fence_proxy_async_smem();  // generic smem writes -> visible to the async (TMA) proxy
     __syncthreads();

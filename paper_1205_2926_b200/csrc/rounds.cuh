@@ -91,7 +91,10 @@ template <int LOGN, int LE, int ra, int rb> __host__ __device__ constexpr bool w
 // only for callers that multiply every output by a twiddle next (the four-step column pass), since a
 // Shoup product takes any T < beta and returns [0,2p) -- the two corrections of P:226's W = 1
 // butterfly are then redundant.
-template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3, bool LAZY_LAST = false>
+// NC: the thread holds NC copies of its G groups (v[k G S + q S + h], k < NC) at the same positions
+// of NC different transforms (the column pass's adjacent columns), so each twiddle load serves NC
+// butterflies.
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int BF = 3, bool LAZY_LAST = false, int NC = 1>
 __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* __restrict__ tw, const Mod<W>& m) {
   NTT_AUDIT_STRESS();  // audit build only: per-warp random delay (race stress)
   constexpr int S = 1 << SR;
@@ -110,11 +113,14 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
         W w = 1, wp = 0;
         if (!unit) ldtw_bf<W, BF>(tw, (uint32_t)(off + hh * D + c[q]), w, wp);
 #pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (LAZY_LAST && BF != 2 && w1) bfly_alg3_w1_lazy<W>(v[q * S + h], v[q * S + h + half], m.p2);
-          else if (unit) bfly_fwd_w1<W, BF>(v[q * S + h], v[q * S + h + half], m);
-          else bfly_fwd<W, PLO1, BF>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          W* u = v + k * G * S + q * S;
+          if (LAZY_LAST && BF != 2 && w1) bfly_alg3_w1_lazy<W>(u[h], u[h + half], m.p2);
+          else if (unit) bfly_fwd_w1<W, BF>(u[h], u[h + half], m);
+          else bfly_fwd<W, PLO1, BF>(u[h], u[h + half], w, wp, m);
         }
       }
     }
@@ -123,7 +129,7 @@ __device__ __forceinline__ void dif_round(W* v, const int* c, const TwPair<W>* _
 
 // Inverse round: the same stages run backwards, Algorithm 4 with the twiddles
 // zeta_i^{-k}, read as their negations from the forward table (inv_index, bfly_alg4n).
-template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1>
+template <class W, int LOGN, int SR, int LEVEL, int G, bool PLO1, int NC = 1>
 __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* __restrict__ twi, const Mod<W>& m) {
   NTT_AUDIT_STRESS();
   constexpr int S = 1 << SR;
@@ -147,10 +153,13 @@ __device__ __forceinline__ void dit_round(W* v, const int* c, const TwPair<W>* _
         // negated twiddle -zeta^{-k} = zeta^{m - k} from the forward table (inv_index)
         if (!unit) ldtw<W>(tq[q], (uint32_t)(off + ((1 << LOGN) >> (LEVEL + j + 1)) - hh * D), w, wp);
 #pragma unroll
+        for (int k = 0; k < NC; ++k)
+#pragma unroll
         for (int b = 0; b < (1 << j); ++b) {
           const int h = b * 2 * half + hh;
-          if (unit) bfly_alg4_w1<W>(v[q * S + h], v[q * S + h + half], m.p2);
-          else bfly_alg4n<W, PLO1>(v[q * S + h], v[q * S + h + half], w, wp, m);
+          W* u = v + k * G * S + q * S;
+          if (unit) bfly_alg4_w1<W>(u[h], u[h + half], m.p2);
+          else bfly_alg4n<W, PLO1>(u[h], u[h + half], w, wp, m);
         }
       }
     }
